@@ -1,0 +1,153 @@
+/*
+ * q8g_b200.h — C ABI of the B200-native quantized u8 x s8 -> s32 GEMM with
+ * fused requantization (the FBGEMM hot path, arXiv 2101.05615).
+ *
+ * This is the drop-in boundary.  Each entry point replaces one reference
+ * interface (cited file:line are under /root/reference/proj/include/q8gemm/
+ * unless noted).  Plain pointers and sizes only; no exceptions cross the ABI:
+ * every call returns a status (Q8G_OK == 0) and sets a thread-local message
+ * readable with q8g_last_error().
+ *
+ * Pointer conventions: arguments named *_dev are device pointers on the
+ * packed handle's device; *_host are host pointers.  Matrices are row-major
+ * with an explicit leading dimension in elements (MatrixView, matrix.hpp:56-68).
+ * `stream` is a cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef Q8G_B200_H
+#define Q8G_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define Q8G_OK 0
+#define Q8G_EINVAL 1 /* std::invalid_argument in the reference (engine.hpp:66-84) */
+#define Q8G_ENOMEM 2
+#define Q8G_ECUDA 3
+#define Q8G_ENOTSUP 4
+
+#define Q8G_ROUND_REF 0     /* quant.hpp:127-133: fp64 multiply, round half away */
+#define Q8G_ROUND_F32_RNE 1 /* fp32 multiply, round to nearest even (BASELINE)   */
+
+typedef struct q8g_packed_b q8g_packed_b;     /* PackedWeight (pack.hpp:63-79) */
+typedef struct q8g_epilogue q8g_epilogue;     /* folded OutputPipeline (pipeline.hpp:57-128) */
+typedef struct q8g_kernel_cache q8g_kernel_cache; /* KernelCache (dispatch.hpp:92-146) */
+typedef struct q8g_dw_filter q8g_dw_filter;   /* new: prepacked depthwise filter */
+
+/* BlockingParams (pack.hpp:15-38).  Kept for API compatibility: the packed
+ * layout is the tcgen05 K-major 128B-swizzled layout whatever the blocking. */
+typedef struct q8g_blocking {
+    int mcb, ncb, kcb, mr, nr;
+} q8g_blocking;
+
+/* RequantParams (quant.hpp:36-43) + the Requantize stage (pipeline.hpp:33-36),
+ * extended with per-output-channel zero point / scale and a rounding mode. */
+typedef struct q8g_requant_params {
+    double multiplier;  /* per-tensor multiplier (> 0) */
+    int32_t zp_a, zp_b, zp_c;
+    int32_t k_total;    /* K of the GEMM (quant.hpp:41) */
+    const int32_t* bias_host;             /* N entries or NULL (quant.hpp:42) */
+    const int32_t* zp_b_per_channel_host; /* N entries or NULL -> zp_b */
+    const float* multiplier_f32_per_channel_host;   /* N or NULL -> (float)multiplier */
+    const double* multiplier_per_channel_host;      /* N or NULL -> multiplier (REF) */
+    const int32_t* col_offsets_host;      /* N or NULL -> the packed B's own colsums */
+    int rounding;       /* Q8G_ROUND_REF or Q8G_ROUND_F32_RNE */
+    int relu;           /* ReluQuantized stage precedes Requantize (pipeline.hpp:31,51-53) */
+} q8g_requant_params;
+
+/* ---- library / errors ---- */
+const char* q8g_last_error(void);
+int q8g_version(void);
+/* number of CUDA kernels this library has launched in this process */
+uint64_t q8g_launch_count(void);
+
+/* ---- blocking (dispatch.hpp:17-30, pack.hpp:24-37) ---- */
+int q8g_blocking_defaults(q8g_blocking* out);
+int q8g_blocking_validate(const q8g_blocking* bp);
+int q8g_select_blocking(int m, int n, int k, const q8g_blocking* defaults, q8g_blocking* out);
+/* engine.hpp:40-47 partition_stripes */
+int q8g_partition_stripes(int num_blocks, int thread_id, int num_threads, int* begin, int* end);
+
+/* ---- weight prepack (pack.hpp:146-196 prepack_weights) ---- */
+/* b_host: K x N int8 row-major (ldb >= N).  Packs on `device` into the
+ * tcgen05 K-major SW128 layout and computes int32 column sums + max_abs. */
+int q8g_pack_b(const int8_t* b_host, int k, int n, int ldb, const q8g_blocking* bp, int device,
+               q8g_packed_b** out);
+/* same from a device-resident B (on `device`), stream-ordered */
+int q8g_pack_b_device(const int8_t* b_dev, int k, int n, int ldb, const q8g_blocking* bp,
+                      int device, void* stream, q8g_packed_b** out);
+/* copy of an immutable packed weight onto another device (row-sharded multi-GPU) */
+int q8g_packed_b_replicate(const q8g_packed_b* src, int device, q8g_packed_b** out);
+int q8g_packed_b_info(const q8g_packed_b* pb, int* k, int* n, int* max_abs, int* device);
+int q8g_packed_b_blocking(const q8g_packed_b* pb, q8g_blocking* out);
+/* ColOffsets over full K (quant.hpp:98-110), N entries */
+int q8g_packed_b_col_offsets(const q8g_packed_b* pb, int32_t* out_host);
+/* test-only inverse (pack.hpp:199-225 unpack_weight): K x N into out_host */
+int q8g_unpack_b(const q8g_packed_b* pb, int8_t* out_host, int ldb);
+int q8g_free_packed_b(q8g_packed_b* pb);
+
+/* ---- output pipeline (pipeline.hpp:57-128) ---- */
+/* Folds a validated [BiasAdd?][ReluQuantized?] Requantize pipeline into a
+ * device-resident per-column table: c[j] = bias[j] + bias_add[j]
+ * - zp_a*colsum[j] + K*zp_a*zp_b[j] ("combined with column
+ * offsets"), zp_b[j], multiplier[j].  bias_add_host is the BiasAdd stage
+ * (pipeline.hpp:27-29) or NULL. */
+int q8g_epilogue_create(const q8g_packed_b* pb, const q8g_requant_params* p,
+                        const int32_t* bias_add_host, q8g_epilogue** out);
+int q8g_epilogue_free(q8g_epilogue* ep);
+
+/* ---- dispatch cache (dispatch.hpp:92-146) ---- */
+int q8g_kernel_cache_create(int generic_only, q8g_kernel_cache** out);
+int q8g_kernel_cache_free(q8g_kernel_cache* kc);
+uint64_t q8g_kernel_cache_build_count(const q8g_kernel_cache* kc);
+/* tile kind chosen for a shape: 0 generic CUDA-core, 1 tcgen05 small-M
+ * (cluster multicast), 2 tcgen05 large-M persistent */
+int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, int* tile_kind);
+
+/* ---- GEMM (engine.hpp:59-169 execute_gemm) ----
+ * Computes output rows [row_begin, row_end) of C = requant(A x B): one
+ * worker's stripe (row_begin=0,row_end=M for the whole matrix).  A is M x K
+ * u8 (lda), C is M x N (ldc).  `cache` NULL = the process cache. */
+int q8g_gemm_u8s8_requant(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                          const q8g_epilogue* ep, uint8_t* c_dev, int ldc, int row_begin,
+                          int row_end, q8g_kernel_cache* cache, void* stream);
+/* WriteRawI32 writer (pipeline.hpp:38,191-198); bias_add_dev = optional
+ * BiasAdd stage (N int32, device) or NULL */
+int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                          const int32_t* bias_add_dev, int32_t* c_dev, int ldc, int row_begin,
+                          int row_end, q8g_kernel_cache* cache, void* stream);
+/* Host-buffer convenience (the reference calling convention: host views).
+ * Stages A to the device, runs, and copies C back, synchronously. */
+int q8g_gemm_u8s8_requant_host(const uint8_t* a_host, int m, int k, int lda,
+                               const q8g_packed_b* pb, const q8g_epilogue* ep, uint8_t* c_host,
+                               int ldc, int row_begin, int row_end, void* stream);
+int q8g_gemm_u8s8_raw_i32_host(const uint8_t* a_host, int m, int k, int lda,
+                               const q8g_packed_b* pb, int32_t* c_host, int ldc, int row_begin,
+                               int row_end, void* stream);
+
+/* ---- conv 3x3, stride 1, pad 1, NHWC (new) ----
+ * x: [nb][h][w][c] u8 (device), padding value = zp_a of the epilogue.
+ * pw: the weight [3][3][c][oc] packed as a K=9c x N=oc matrix.
+ * y: [nb][h][w][oc] u8.  Images [img_begin, img_end) are computed. */
+int q8g_conv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
+                          const q8g_packed_b* pw, const q8g_epilogue* ep, uint8_t* y_dev,
+                          int img_begin, int img_end, void* stream);
+int q8g_conv3x3_u8s8_nhwc_raw_i32(const uint8_t* x_dev, int nb, int h, int w, int c,
+                                  int32_t zp_a, const q8g_packed_b* pw, int32_t* y_dev,
+                                  int img_begin, int img_end, void* stream);
+
+/* ---- depthwise 3x3, stride 1, pad 1, NHWC (new) ----
+ * w_host: [3][3][c] s8.  Requant params are per channel (k_total = 9). */
+int q8g_dw_filter_create(const int8_t* w_host, int c, const q8g_requant_params* p, int device,
+                         q8g_dw_filter** out);
+int q8g_dw_filter_free(q8g_dw_filter* f);
+int q8g_dwconv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
+                            const q8g_dw_filter* f, uint8_t* y_dev, int img_begin, int img_end,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* Q8G_B200_H */

@@ -1,0 +1,617 @@
+// abi.cu — the extern "C" boundary (include/q8g_b200.h).
+//
+// Validation mirrors the reference's std::invalid_argument conditions
+// (engine.hpp:63-84, pack.hpp:24-37, pipeline.hpp:66-102, dispatch.hpp:17-30)
+// and maps them to Q8G_EINVAL with the same message text.  No exception
+// crosses this file's functions.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "q8g_internal.cuh"
+
+namespace q8g {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+    return Q8G_ECUDA;
+}
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int sm_count(int device) {
+    static int cache[64] = {0};
+    if (device >= 0 && device < 64 && cache[device]) return cache[device];
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    if (device >= 0 && device < 64) cache[device] = v;
+    return v;
+}
+
+static int validate_blocking(const q8g_blocking& bp) {
+    if (bp.mcb < 1 || bp.ncb < 1 || bp.kcb < 1 || bp.mr < 1 || bp.nr < 1)
+        return fail(Q8G_EINVAL, "BlockingParams: all sizes must be >= 1");
+    if (bp.mcb % bp.mr != 0) return fail(Q8G_EINVAL, "BlockingParams: mcb must be a multiple of mr");
+    if (bp.ncb % bp.nr != 0) return fail(Q8G_EINVAL, "BlockingParams: ncb must be a multiple of nr");
+    if (bp.kcb % 2 != 0)
+        return fail(Q8G_EINVAL, "BlockingParams: kcb must be even (k is consumed in pairs)");
+    return Q8G_OK;
+}
+
+static q8g_kernel_cache& process_cache() {
+    static q8g_kernel_cache* c = new q8g_kernel_cache();
+    return *c;
+}
+
+// Shape class -> tile kind, memoized (dispatch.hpp:60-75 classify_shape,
+// 117-140 build).  `aligned` = TMA can address A (16B-aligned base, lda%16==0).
+static int resolve_tile(q8g_kernel_cache* kc, int rows, int n, int k, bool aligned) {
+    ShapeKey key;
+    key.m_class = rows <= 128 ? 0 : 1;
+    key.n_class = n <= 32 ? 0 : 1;
+    key.k_class = k % 16 == 0 ? 0 : 1;
+    key.align = aligned ? 1 : 0;
+    std::lock_guard<std::mutex> lock(kc->mu);
+    auto it = kc->table.find(key);
+    if (it != kc->table.end()) return it->second;
+    ++kc->builds;
+    int kind = kGeneric;
+    if (!kc->generic_only && key.align && key.k_class == 0)
+        kind = key.m_class == 0 ? kSmallM : kLargeM;
+    kc->table.emplace(key, kind);
+    return kind;
+}
+
+static bool a_is_tma_aligned(const void* a, int lda) {
+    return ((uintptr_t)a % 16 == 0) && (lda % 16 == 0);
+}
+
+}  // namespace q8g
+
+using namespace q8g;
+
+extern "C" {
+
+const char* q8g_last_error(void) { return g_last_error.c_str(); }
+int q8g_version(void) { return 1; }
+uint64_t q8g_launch_count(void) { return g_launches.load(); }
+
+int q8g_blocking_defaults(q8g_blocking* out) {
+    if (!out) return fail(Q8G_EINVAL, "null output");
+    *out = q8g_blocking{56, 32, 256, 14, 32};  // pack.hpp:16-20
+    return Q8G_OK;
+}
+
+int q8g_blocking_validate(const q8g_blocking* bp) {
+    if (!bp) return fail(Q8G_EINVAL, "null blocking");
+    return validate_blocking(*bp);
+}
+
+int q8g_select_blocking(int m, int n, int k, const q8g_blocking* defaults, q8g_blocking* out) {
+    if (!defaults || !out) return fail(Q8G_EINVAL, "null blocking");
+    int rc = validate_blocking(*defaults);
+    if (rc) return rc;
+    if (m < 1 || n < 1 || k < 1) return fail(Q8G_EINVAL, "select_blocking: dimensions must be >= 1");
+    q8g_blocking bp = *defaults;
+    bp.mr = std::min(defaults->mr, m);
+    bp.nr = std::min(defaults->nr, n);
+    bp.mcb = std::min(defaults->mcb, round_up_i(m, bp.mr));
+    bp.ncb = std::min(defaults->ncb, round_up_i(n, bp.nr));
+    bp.kcb = std::min(defaults->kcb, round_up_i(k, 2));
+    rc = validate_blocking(bp);
+    if (rc) return rc;
+    *out = bp;
+    return Q8G_OK;
+}
+
+int q8g_partition_stripes(int num_blocks, int thread_id, int num_threads, int* begin, int* end) {
+    if (num_threads < 1 || thread_id < 0 || thread_id >= num_threads)
+        return fail(Q8G_EINVAL, "execute_gemm: thread_id must be in [0, num_threads)");
+    if (num_blocks < 0 || !begin || !end) return fail(Q8G_EINVAL, "partition_stripes: bad arguments");
+    const int base = num_blocks / num_threads, rem = num_blocks % num_threads;
+    *begin = thread_id * base + std::min(thread_id, rem);
+    *end = *begin + base + (thread_id < rem ? 1 : 0);
+    return Q8G_OK;
+}
+
+// ---------------------------------------------------------------- pack
+
+static int pack_common(const int8_t* b, bool b_on_device, int k, int n, int ldb,
+                       const q8g_blocking* bp, int device, cudaStream_t s, q8g_packed_b** out) {
+    if (!out) return fail(Q8G_EINVAL, "null output handle");
+    *out = nullptr;
+    q8g_blocking blk;
+    q8g_blocking_defaults(&blk);
+    if (bp) blk = *bp;
+    int rc = validate_blocking(blk);
+    if (rc) return rc;
+    if (k < 1 || n < 1) return fail(Q8G_EINVAL, "prepack_weights: matrix must be non-empty");
+    if (!b || ldb < n) return fail(Q8G_EINVAL, "prepack_weights: bad B pointer or ldb < N");
+    DeviceGuard dg(device);
+    auto* pb = new (std::nothrow) q8g_packed_b();
+    if (!pb) return fail(Q8G_ENOMEM, "out of host memory");
+    pb->device = device;
+    pb->k = k;
+    pb->n = n;
+    pb->kp = round_up_i(k, kKBlock);
+    pb->np = round_up_i(n, kNPad);
+    pb->blocking = blk;
+    int* d_max = nullptr;
+    const int8_t* d_b = b;
+    int8_t* staged = nullptr;
+    auto cleanup = [&](int code) {
+        if (staged) cudaFree(staged);
+        if (d_max) cudaFree(d_max);
+        if (code != Q8G_OK) q8g_free_packed_b(pb);
+        return code;
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&pb->data, (size_t)pb->kp * pb->np)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMalloc(packed B)"));
+    if ((e = cudaMalloc(&pb->colsum_dev, sizeof(int32_t) * pb->np)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMalloc(colsum)"));
+    if ((e = cudaMalloc(&d_max, sizeof(int))) != cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMalloc(max_abs)"));
+    if (!b_on_device) {
+        if ((e = cudaMalloc(&staged, (size_t)k * ldb)) != cudaSuccess)
+            return cleanup(cuda_fail(e, "cudaMalloc(staged B)"));
+        if ((e = cudaMemcpyAsync(staged, b, (size_t)(k - 1) * ldb + n, cudaMemcpyHostToDevice, s)) !=
+            cudaSuccess)
+            return cleanup(cuda_fail(e, "cudaMemcpyAsync(B)"));
+        d_b = staged;
+    }
+    if ((e = launch_pack_b(d_b, k, n, ldb, pb->data, pb->kp, pb->np, pb->colsum_dev, d_max, s)) !=
+        cudaSuccess)
+        return cleanup(cuda_fail(e, "pack_b kernel"));
+    pb->colsum_host = (int32_t*)malloc(sizeof(int32_t) * pb->np);
+    if ((e = cudaMemcpyAsync(pb->colsum_host, pb->colsum_dev, sizeof(int32_t) * pb->np,
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMemcpyAsync(colsum)"));
+    if ((e = cudaMemcpyAsync(&pb->max_abs, d_max, sizeof(int), cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMemcpyAsync(max_abs)"));
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "pack_b synchronize"));
+    *out = pb;
+    return cleanup(Q8G_OK);
+}
+
+int q8g_pack_b(const int8_t* b_host, int k, int n, int ldb, const q8g_blocking* bp, int device,
+               q8g_packed_b** out) {
+    return pack_common(b_host, false, k, n, ldb, bp, device, nullptr, out);
+}
+
+int q8g_pack_b_device(const int8_t* b_dev, int k, int n, int ldb, const q8g_blocking* bp,
+                      int device, void* stream, q8g_packed_b** out) {
+    return pack_common(b_dev, true, k, n, ldb, bp, device, (cudaStream_t)stream, out);
+}
+
+int q8g_packed_b_replicate(const q8g_packed_b* src, int device, q8g_packed_b** out) {
+    if (!src || !out) return fail(Q8G_EINVAL, "null handle");
+    DeviceGuard dg(device);
+    auto* pb = new (std::nothrow) q8g_packed_b(*src);
+    if (!pb) return fail(Q8G_ENOMEM, "out of host memory");
+    pb->device = device;
+    pb->data = nullptr;
+    pb->colsum_dev = nullptr;
+    pb->colsum_host = (int32_t*)malloc(sizeof(int32_t) * src->np);
+    memcpy(pb->colsum_host, src->colsum_host, sizeof(int32_t) * src->np);
+    cudaError_t e;
+    if ((e = cudaMalloc(&pb->data, (size_t)pb->kp * pb->np)) != cudaSuccess ||
+        (e = cudaMalloc(&pb->colsum_dev, sizeof(int32_t) * pb->np)) != cudaSuccess) {
+        q8g_free_packed_b(pb);
+        return cuda_fail(e, "cudaMalloc(replica)");
+    }
+    if ((e = cudaMemcpyPeer(pb->data, device, src->data, src->device, (size_t)pb->kp * pb->np)) !=
+            cudaSuccess ||
+        (e = cudaMemcpy(pb->colsum_dev, pb->colsum_host, sizeof(int32_t) * pb->np,
+                        cudaMemcpyHostToDevice)) != cudaSuccess) {
+        q8g_free_packed_b(pb);
+        return cuda_fail(e, "replicate copy");
+    }
+    *out = pb;
+    return Q8G_OK;
+}
+
+int q8g_packed_b_info(const q8g_packed_b* pb, int* k, int* n, int* max_abs, int* device) {
+    if (!pb) return fail(Q8G_EINVAL, "null handle");
+    if (k) *k = pb->k;
+    if (n) *n = pb->n;
+    if (max_abs) *max_abs = pb->max_abs;
+    if (device) *device = pb->device;
+    return Q8G_OK;
+}
+
+int q8g_packed_b_blocking(const q8g_packed_b* pb, q8g_blocking* out) {
+    if (!pb || !out) return fail(Q8G_EINVAL, "null handle");
+    *out = pb->blocking;
+    return Q8G_OK;
+}
+
+int q8g_packed_b_col_offsets(const q8g_packed_b* pb, int32_t* out_host) {
+    if (!pb || !out_host) return fail(Q8G_EINVAL, "null handle");
+    memcpy(out_host, pb->colsum_host, sizeof(int32_t) * pb->n);
+    return Q8G_OK;
+}
+
+int q8g_unpack_b(const q8g_packed_b* pb, int8_t* out_host, int ldb) {
+    if (!pb || !out_host || ldb < pb->n) return fail(Q8G_EINVAL, "unpack_weight: bad arguments");
+    DeviceGuard dg(pb->device);
+    int8_t* d = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&d, (size_t)pb->k * ldb)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    e = launch_unpack_b(pb->data, pb->k, pb->n, pb->kp, pb->np, d, ldb, nullptr);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(out_host, d, (size_t)(pb->k - 1) * ldb + pb->n, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "unpack_b");
+    return Q8G_OK;
+}
+
+int q8g_free_packed_b(q8g_packed_b* pb) {
+    if (!pb) return Q8G_OK;
+    DeviceGuard dg(pb->device);
+    if (pb->data) cudaFree(pb->data);
+    if (pb->colsum_dev) cudaFree(pb->colsum_dev);
+    free(pb->colsum_host);
+    delete pb;
+    return Q8G_OK;
+}
+
+// ---------------------------------------------------------------- epilogue
+
+static int build_records(int n, int np, int32_t k_total, const q8g_requant_params* p,
+                         const int32_t* colsum, const int32_t* bias_add, std::vector<EpiRecord>& rec,
+                         bool& need_rowsum) {
+    if (p->rounding != Q8G_ROUND_REF && p->rounding != Q8G_ROUND_F32_RNE)
+        return fail(Q8G_EINVAL, "Requantize: unknown rounding mode");
+    if (!(p->multiplier > 0) && !p->multiplier_f32_per_channel_host &&
+        !p->multiplier_per_channel_host)
+        return fail(Q8G_EINVAL, "OutputPipeline: Requantize multiplier must be positive");
+    if (k_total < 1) return fail(Q8G_EINVAL, "OutputPipeline: Requantize k_total must be >= 1");
+    if (p->zp_c > (1 << 30) || p->zp_c < -(1 << 30))
+        return fail(Q8G_EINVAL, "Requantize: |zp_c| must be <= 2^30");
+    rec.assign(np, EpiRecord{});
+    need_rowsum = false;
+    for (int j = 0; j < n; ++j) {
+        const int64_t zpb = p->zp_b_per_channel_host ? p->zp_b_per_channel_host[j] : p->zp_b;
+        const int64_t bias = (p->bias_host ? p->bias_host[j] : 0) + (bias_add ? bias_add[j] : 0);
+        const int64_t c = bias - (int64_t)p->zp_a * colsum[j] + (int64_t)k_total * p->zp_a * zpb;
+        rec[j].c = (int32_t)(uint32_t)(uint64_t)c;  // wraps mod 2^32 (see requant.cuh)
+        rec[j].zpb = (int32_t)zpb;
+        if (zpb != 0) need_rowsum = true;
+        if (p->rounding == Q8G_ROUND_F32_RNE) {
+            const float mf = p->multiplier_f32_per_channel_host
+                                 ? p->multiplier_f32_per_channel_host[j]
+                                 : (float)p->multiplier;
+            if (!(mf > 0)) return fail(Q8G_EINVAL, "OutputPipeline: Requantize multiplier must be positive");
+            rec[j].md = 0.0;
+            rec[j].mf = mf;
+        } else {
+            const double md =
+                p->multiplier_per_channel_host ? p->multiplier_per_channel_host[j] : p->multiplier;
+            if (!(md > 0)) return fail(Q8G_EINVAL, "OutputPipeline: Requantize multiplier must be positive");
+            rec[j].md = md;
+        }
+    }
+    return Q8G_OK;
+}
+
+int q8g_epilogue_create(const q8g_packed_b* pb, const q8g_requant_params* p,
+                        const int32_t* bias_add_host, q8g_epilogue** out) {
+    if (!pb || !p || !out) return fail(Q8G_EINVAL, "null argument");
+    *out = nullptr;
+    // exactness bound of the int32 adjust (requant.cuh): |adj| <= 255*255*K + |bias|
+    // < 2^31 for K <= 32768 and |bias| < 2^24
+    if (pb->k > 32768)
+        return fail(Q8G_EINVAL, "Requantize: K too large for an exact int32 accumulator");
+    const int32_t* colsum = p->col_offsets_host ? p->col_offsets_host : pb->colsum_host;
+    std::vector<EpiRecord> rec;
+    bool need_rowsum = false;
+    int rc = build_records(pb->n, pb->np, p->k_total, p, colsum, bias_add_host, rec, need_rowsum);
+    if (rc) return rc;
+    DeviceGuard dg(pb->device);
+    auto* ep = new (std::nothrow) q8g_epilogue();
+    if (!ep) return fail(Q8G_ENOMEM, "out of host memory");
+    ep->device = pb->device;
+    ep->n = pb->n;
+    ep->np = pb->np;
+    ep->k_total = p->k_total;
+    ep->zp_a = p->zp_a;
+    ep->zp_c = p->zp_c;
+    ep->rounding = p->rounding;
+    ep->relu = p->relu ? 1 : 0;
+    ep->need_rowsum = need_rowsum;
+    cudaError_t e;
+    if ((e = cudaMalloc(&ep->rec, sizeof(EpiRecord) * pb->np)) != cudaSuccess ||
+        (e = cudaMemcpy(ep->rec, rec.data(), sizeof(EpiRecord) * pb->np, cudaMemcpyHostToDevice)) !=
+            cudaSuccess) {
+        q8g_epilogue_free(ep);
+        return cuda_fail(e, "epilogue table");
+    }
+    *out = ep;
+    return Q8G_OK;
+}
+
+int q8g_epilogue_free(q8g_epilogue* ep) {
+    if (!ep) return Q8G_OK;
+    DeviceGuard dg(ep->device);
+    if (ep->rec) cudaFree(ep->rec);
+    delete ep;
+    return Q8G_OK;
+}
+
+// ---------------------------------------------------------------- dispatch cache
+
+int q8g_kernel_cache_create(int generic_only, q8g_kernel_cache** out) {
+    if (!out) return fail(Q8G_EINVAL, "null output");
+    *out = new (std::nothrow) q8g_kernel_cache();
+    if (!*out) return fail(Q8G_ENOMEM, "out of host memory");
+    (*out)->generic_only = generic_only != 0;
+    return Q8G_OK;
+}
+
+int q8g_kernel_cache_free(q8g_kernel_cache* kc) {
+    if (kc && kc != &process_cache()) delete kc;
+    return Q8G_OK;
+}
+
+uint64_t q8g_kernel_cache_build_count(const q8g_kernel_cache* kc) {
+    auto* c = const_cast<q8g_kernel_cache*>(kc ? kc : &process_cache());
+    std::lock_guard<std::mutex> lock(c->mu);
+    return c->builds;
+}
+
+int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, int* tile_kind) {
+    if (!tile_kind) return fail(Q8G_EINVAL, "null output");
+    *tile_kind = resolve_tile(kc ? kc : &process_cache(), m, n, k, lda % 16 == 0);
+    return Q8G_OK;
+}
+
+// ---------------------------------------------------------------- GEMM
+
+static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed_b* pb,
+                       const q8g_epilogue* ep, const int32_t* bias_add, void* c, int ldc,
+                       int row_begin, int row_end, q8g_kernel_cache* cache, cudaStream_t s,
+                       bool raw) {
+    if (!pb) return fail(Q8G_EINVAL, "execute_gemm: null packed weight");
+    if (k != pb->k) return fail(Q8G_EINVAL, "execute_gemm: A columns must equal the packed weight K");
+    if (m < 1 || lda < k || ldc < pb->n || !a || !c)
+        return fail(Q8G_EINVAL, "execute_gemm: output must be M x N");
+    if (row_begin < 0 || row_end > m || row_begin > row_end)
+        return fail(Q8G_EINVAL, "execute_gemm: row stripe out of range");
+    if (!raw) {
+        if (!ep) return fail(Q8G_EINVAL, "pipeline writer does not match the output element type");
+        if (ep->n != pb->n || ep->device != pb->device)
+            return fail(Q8G_EINVAL, "execute_gemm: epilogue was built for another packed weight");
+    }
+    if (row_begin == row_end) return Q8G_OK;
+    DeviceGuard dg(pb->device);
+    GemmArgs g;
+    g.rows = row_end - row_begin;
+    g.k = k;
+    g.lda = lda;
+    g.a = a + (size_t)row_begin * lda;
+    g.pb = pb;
+    g.ep = ep;
+    g.bias_add = bias_add;
+    g.raw = raw;
+    g.ldc = ldc;
+    g.c = raw ? (void*)((int32_t*)c + (size_t)row_begin * ldc)
+              : (void*)((uint8_t*)c + (size_t)row_begin * ldc);
+    const int kind = resolve_tile(cache ? cache : &process_cache(), g.rows, pb->n, k,
+                                  a_is_tma_aligned(g.a, lda));
+    cudaError_t e;
+    if (kind != kGeneric && tc_supported(g))
+        e = launch_gemm_tc(g, kind, s);
+    else
+        e = launch_gemm_simt(g, s);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
+    return Q8G_OK;
+}
+
+int q8g_gemm_u8s8_requant(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                          const q8g_epilogue* ep, uint8_t* c_dev, int ldc, int row_begin,
+                          int row_end, q8g_kernel_cache* cache, void* stream) {
+    return gemm_common(a_dev, m, k, lda, pb, ep, nullptr, c_dev, ldc, row_begin, row_end, cache,
+                       (cudaStream_t)stream, false);
+}
+
+int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                          const int32_t* bias_add_dev, int32_t* c_dev, int ldc, int row_begin,
+                          int row_end, q8g_kernel_cache* cache, void* stream) {
+    return gemm_common(a_dev, m, k, lda, pb, nullptr, bias_add_dev, c_dev, ldc, row_begin,
+                       row_end, cache, (cudaStream_t)stream, true);
+}
+
+}  // extern "C"
+
+template <typename OutT>
+static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_packed_b* pb,
+                     const q8g_epilogue* ep, OutT* c_host, int ldc, int row_begin, int row_end,
+                     cudaStream_t s, bool raw) {
+    if (!pb || !a_host || !c_host) return fail(Q8G_EINVAL, "execute_gemm: null argument");
+    if (row_begin < 0 || row_end > m || row_begin > row_end)
+        return fail(Q8G_EINVAL, "execute_gemm: row stripe out of range");
+    if (k != pb->k) return fail(Q8G_EINVAL, "execute_gemm: A columns must equal the packed weight K");
+    if (lda < k || ldc < pb->n) return fail(Q8G_EINVAL, "execute_gemm: output must be M x N");
+    const int rows = row_end - row_begin;
+    if (rows == 0) return Q8G_OK;
+    DeviceGuard dg(pb->device);
+    uint8_t* d_a = nullptr;
+    OutT* d_c = nullptr;
+    const int lda_d = round_up_i(k, 16), ldc_d = pb->n;
+    cudaError_t e;
+    if ((e = cudaMalloc(&d_a, (size_t)rows * lda_d)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(A)");
+    if ((e = cudaMalloc(&d_c, sizeof(OutT) * (size_t)rows * ldc_d)) != cudaSuccess) {
+        cudaFree(d_a);
+        return cuda_fail(e, "cudaMalloc(C)");
+    }
+    int rc = Q8G_OK;
+    e = cudaMemcpy2DAsync(d_a, lda_d, a_host + (size_t)row_begin * lda, lda, k, rows,
+                          cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "H2D A");
+    if (!rc) {
+        if (raw)
+            rc = q8g_gemm_u8s8_raw_i32(d_a, rows, k, lda_d, pb, nullptr, (int32_t*)d_c, ldc_d, 0,
+                                       rows, nullptr, s);
+        else
+            rc = q8g_gemm_u8s8_requant(d_a, rows, k, lda_d, pb, ep, (uint8_t*)d_c, ldc_d, 0, rows,
+                                       nullptr, s);
+    }
+    if (!rc) {
+        e = cudaMemcpy2DAsync(c_host + (size_t)row_begin * ldc, sizeof(OutT) * ldc, d_c,
+                              sizeof(OutT) * ldc_d, sizeof(OutT) * pb->n, rows,
+                              cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H C");
+    }
+    cudaFree(d_a);
+    cudaFree(d_c);
+    return rc;
+}
+
+extern "C" {
+
+int q8g_gemm_u8s8_requant_host(const uint8_t* a_host, int m, int k, int lda,
+                               const q8g_packed_b* pb, const q8g_epilogue* ep, uint8_t* c_host,
+                               int ldc, int row_begin, int row_end, void* stream) {
+    if (!ep) return fail(Q8G_EINVAL, "pipeline writer does not match the output element type");
+    return gemm_host<uint8_t>(a_host, m, k, lda, pb, ep, c_host, ldc, row_begin, row_end,
+                              (cudaStream_t)stream, false);
+}
+
+int q8g_gemm_u8s8_raw_i32_host(const uint8_t* a_host, int m, int k, int lda,
+                               const q8g_packed_b* pb, int32_t* c_host, int ldc, int row_begin,
+                               int row_end, void* stream) {
+    return gemm_host<int32_t>(a_host, m, k, lda, pb, nullptr, c_host, ldc, row_begin, row_end,
+                              (cudaStream_t)stream, true);
+}
+
+// ---------------------------------------------------------------- conv 3x3
+
+static int conv_common(const uint8_t* x, int nb, int h, int w, int c, int32_t zp_a,
+                       const q8g_packed_b* pw, const q8g_epilogue* ep, void* y, int img_begin,
+                       int img_end, cudaStream_t s, bool raw) {
+    if (!pw || !x || !y) return fail(Q8G_EINVAL, "conv3x3: null argument");
+    if (nb < 1 || h < 1 || w < 1 || c < 1) return fail(Q8G_EINVAL, "conv3x3: dimensions must be >= 1");
+    if (pw->k != 9 * c) return fail(Q8G_EINVAL, "conv3x3: packed weight K must equal 9*C");
+    if (img_begin < 0 || img_end > nb || img_begin > img_end)
+        return fail(Q8G_EINVAL, "conv3x3: image range out of bounds");
+    if (!raw && (!ep || ep->n != pw->n))
+        return fail(Q8G_EINVAL, "conv3x3: epilogue does not match the packed weight");
+    if (zp_a < 0 || zp_a > 255) return fail(Q8G_EINVAL, "conv3x3: zp_a must be a u8 value");
+    if (img_begin == img_end) return Q8G_OK;
+    DeviceGuard dg(pw->device);
+    ConvArgs a;
+    const size_t img_px = (size_t)h * w;
+    a.x = x + (size_t)img_begin * img_px * c;
+    a.nb = img_end - img_begin;
+    a.h = h;
+    a.w = w;
+    a.c = c;
+    a.zp_a = zp_a;
+    a.pw = pw;
+    a.ep = ep;
+    a.raw = raw;
+    a.y = raw ? (void*)((int32_t*)y + (size_t)img_begin * img_px * pw->n)
+              : (void*)((uint8_t*)y + (size_t)img_begin * img_px * pw->n);
+    cudaError_t e = launch_conv3x3(a, s);
+    if (e != cudaSuccess) return cuda_fail(e, "conv3x3 launch");
+    return Q8G_OK;
+}
+
+int q8g_conv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
+                          const q8g_packed_b* pw, const q8g_epilogue* ep, uint8_t* y_dev,
+                          int img_begin, int img_end, void* stream) {
+    if (!ep) return fail(Q8G_EINVAL, "conv3x3: null epilogue");
+    return conv_common(x_dev, nb, h, w, c, ep->zp_a, pw, ep, y_dev, img_begin, img_end,
+                       (cudaStream_t)stream, false);
+}
+
+int q8g_conv3x3_u8s8_nhwc_raw_i32(const uint8_t* x_dev, int nb, int h, int w, int c,
+                                  int32_t zp_a, const q8g_packed_b* pw, int32_t* y_dev,
+                                  int img_begin, int img_end, void* stream) {
+    return conv_common(x_dev, nb, h, w, c, zp_a, pw, nullptr, y_dev, img_begin, img_end,
+                       (cudaStream_t)stream, true);
+}
+
+// ---------------------------------------------------------------- depthwise
+
+int q8g_dw_filter_create(const int8_t* w_host, int c, const q8g_requant_params* p, int device,
+                         q8g_dw_filter** out) {
+    if (!w_host || !p || !out || c < 1) return fail(Q8G_EINVAL, "dw_filter: bad arguments");
+    *out = nullptr;
+    if (p->rounding != Q8G_ROUND_F32_RNE)
+        return fail(Q8G_ENOTSUP, "dwconv3x3: only F32_RNE requantization is supported");
+    if (p->zp_a < 0 || p->zp_a > 255) return fail(Q8G_EINVAL, "dwconv3x3: zp_a must be a u8 value");
+    std::vector<int32_t> wsum(c, 0);
+    for (int t = 0; t < 9; ++t)
+        for (int ch = 0; ch < c; ++ch) wsum[ch] += w_host[t * c + ch];
+    std::vector<EpiRecord> rec;
+    bool need_rowsum = false;
+    int rc = build_records(c, c, 9, p, wsum.data(), nullptr, rec, need_rowsum);
+    if (rc) return rc;
+    DeviceGuard dg(device);
+    auto* f = new (std::nothrow) q8g_dw_filter();
+    if (!f) return fail(Q8G_ENOMEM, "out of host memory");
+    f->device = device;
+    f->c = c;
+    f->zp_a = p->zp_a;
+    f->zp_c = p->zp_c;
+    f->relu = p->relu ? 1 : 0;
+    cudaError_t e;
+    if ((e = cudaMalloc(&f->w, (size_t)9 * c)) != cudaSuccess ||
+        (e = cudaMalloc(&f->rec, sizeof(EpiRecord) * c)) != cudaSuccess ||
+        (e = cudaMemcpy(f->w, w_host, (size_t)9 * c, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(f->rec, rec.data(), sizeof(EpiRecord) * c, cudaMemcpyHostToDevice)) !=
+            cudaSuccess) {
+        q8g_dw_filter_free(f);
+        return cuda_fail(e, "dw_filter upload");
+    }
+    *out = f;
+    return Q8G_OK;
+}
+
+int q8g_dw_filter_free(q8g_dw_filter* f) {
+    if (!f) return Q8G_OK;
+    DeviceGuard dg(f->device);
+    if (f->w) cudaFree(f->w);
+    if (f->rec) cudaFree(f->rec);
+    delete f;
+    return Q8G_OK;
+}
+
+int q8g_dwconv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
+                            const q8g_dw_filter* f, uint8_t* y_dev, int img_begin, int img_end,
+                            void* stream) {
+    if (!f || !x_dev || !y_dev) return fail(Q8G_EINVAL, "dwconv3x3: null argument");
+    if (nb < 1 || h < 1 || w < 1 || c < 1) return fail(Q8G_EINVAL, "dwconv3x3: dimensions must be >= 1");
+    if (c != f->c) return fail(Q8G_EINVAL, "dwconv3x3: channel count does not match the filter");
+    if (img_begin < 0 || img_end > nb || img_begin > img_end)
+        return fail(Q8G_EINVAL, "dwconv3x3: image range out of bounds");
+    if (img_begin == img_end) return Q8G_OK;
+    DeviceGuard dg(f->device);
+    const size_t img = (size_t)h * w * c;
+    cudaError_t e = launch_dwconv3x3(x_dev + img_begin * img, img_end - img_begin, h, w, c, f,
+                                     y_dev + img_begin * img, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dwconv3x3 launch");
+    return Q8G_OK;
+}
+
+}  // extern "C"

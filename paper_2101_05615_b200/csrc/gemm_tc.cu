@@ -1,0 +1,475 @@
+// gemm_tc.cu — the hot path: u8 x s8 -> s32 GEMM on the 5th-generation
+// tensor cores (tcgen05.mma kind::i8, int32 accumulators in TMEM) with the
+// requantization back-end fused onto the TMEM -> register -> global drain.
+//
+// Replaces, for the reference (proj/include/q8gemm/):
+//   execute_gemm's five loops (engine.hpp:109-167) + microkernel_i32
+//   (kernel.hpp:42-68, 108-112, 150-153)          -> MMA warp + TMEM
+//   pack_a_with_row_offsets (pack.hpp:83-135)      -> TMA producer (A tile,
+//                                                     swizzled in smem) +
+//                                                     row-sum warps reading it
+//   run_block + Requantize/ReluQuantized/WriteRawI32 (pipeline.hpp:157-210,
+//   quant.hpp:115-133)                             -> epilogue warps
+//
+// One CTA per SM, warp-specialised, persistent over output tiles:
+//   warp 0      TMA producer: A tile (128 rows x 128 B of K) by tensor map
+//               (multicast across a cluster of CN CTAs that share the rows),
+//               B tile (BN channels x 128 B) by one cp.async.bulk of the
+//               pre-swizzled packed weight
+//   warp 1      MMA issuer (one thread): 4 x tcgen05.mma (K=32 each) per stage
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time, requantize, store
+//   warps 8-11  row sums of A (only when some zp_b != 0, pipeline.hpp:114-119)
+// Pipelines: smem stages full/empty (TMA <-> MMA + row sums), TMEM double
+// buffer full/empty (MMA <-> epilogue), row-sum double buffer.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "ptx.cuh"
+#include "q8g_internal.cuh"
+#include "requant.cuh"
+
+namespace q8g {
+namespace {
+
+constexpr int BM = 128;
+constexpr int A_STAGE_BYTES = BM * kKBlock;  // 16 KB
+
+template <int BN, int CN, int STAGES>
+struct TcCfg {
+    static constexpr int B_STAGE_BYTES = BN * kKBlock;
+    static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;  // power of two for BN in {16..256}
+    static constexpr int A_OFF = 0;
+    static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
+    static constexpr int BAR_OFF = B_OFF + STAGES * B_STAGE_BYTES;
+    // barriers: full[S], empty[S], tfull[2], tempty[2], rfull[2], rempty[2]
+    static constexpr int NUM_BARS = 2 * STAGES + 8;
+    static constexpr int RS_OFF = BAR_OFF + NUM_BARS * 8;
+    static constexpr int TMEMPTR_OFF = RS_OFF + 2 * BM * 4;
+    static constexpr int SMEM_BYTES = TMEMPTR_OFF + 16 + 1024;  // + alignment slack
+};
+
+struct TcParams {
+    const int8_t* pb;        // packed B
+    int np, nkb;             // padded N, number of 128-byte k-blocks
+    int n;                   // logical N
+    int rows;                // rows in this stripe
+    int num_m_tiles, num_n_groups;
+    const EpiRecord* rec;
+    int32_t zp_c;
+    int relu;
+    const int32_t* bias_add;  // raw writer only
+    void* c;
+    int ldc;
+};
+
+constexpr int EPI_COLS = 16;  // columns per tcgen05.ld in the epilogue
+
+template <int MODE>
+__device__ __forceinline__ void store_chunk(const TcParams& p, int row, int col0,
+                                            const uint32_t (&v)[EPI_COLS], int32_t rowsum) {
+    // MODE 0: raw int32 (+BiasAdd); 1: requant F32_RNE; 2: requant REF
+    if (MODE == 0) {
+        int32_t* dst = reinterpret_cast<int32_t*>(p.c) + (size_t)row * p.ldc + col0;
+        int32_t out[EPI_COLS];
+#pragma unroll
+        for (int j = 0; j < EPI_COLS; ++j) {
+            int32_t x = (int32_t)v[j];
+            if (p.bias_add && col0 + j < p.n)
+                x = (int32_t)((uint32_t)x + (uint32_t)__ldg(p.bias_add + col0 + j));
+            out[j] = x;
+        }
+        const bool vec = (col0 + EPI_COLS <= p.n) && ((p.ldc & 3) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+        if (vec) {
+#pragma unroll
+            for (int j = 0; j < EPI_COLS; j += 4)
+                *reinterpret_cast<int4*>(dst + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < EPI_COLS; ++j)
+                if (col0 + j < p.n) dst[j] = out[j];
+        }
+    } else {
+        uint32_t packed[EPI_COLS / 4];
+#pragma unroll
+        for (int w = 0; w < EPI_COLS / 4; ++w) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = w * 4 + b;
+                const int4 r4 = __ldg(reinterpret_cast<const int4*>(p.rec + col0 + j));
+                EpiRecord rc;
+                rc.c = r4.x;
+                rc.zpb = r4.y;
+                uint32_t q;
+                const int32_t adj = adjust((int32_t)v[j], rowsum, rc);
+                if (MODE == 1) {
+                    q = requant_f32(adj, __int_as_float(r4.z), p.zp_c, p.relu);
+                } else {
+                    const double md = __hiloint2double(r4.w, r4.z);
+                    q = requant_ref(adj, md, p.zp_c, p.relu);
+                }
+                word |= q << (8 * b);
+            }
+            packed[w] = word;
+        }
+        uint8_t* dst = reinterpret_cast<uint8_t*>(p.c) + (size_t)row * p.ldc + col0;
+        const bool vec = (col0 + EPI_COLS <= p.n) && ((p.ldc & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+        if (vec) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < EPI_COLS; ++j)
+                if (col0 + j < p.n) dst[j] = (uint8_t)(packed[j / 4] >> (8 * (j % 4)));
+        }
+    }
+}
+
+template <int BN, int CN, int STAGES, int MODE, bool RS>
+__global__ void __launch_bounds__(RS ? 384 : 256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const TcParams p) {
+    using Cfg = TcCfg<BN, CN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the SWIZZLE_128B atoms
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    const uint32_t base = (raw_addr + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base - raw_addr);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = CN > 1 ? ptx::cluster_ctarank() : 0;
+    const uint32_t sA = base + Cfg::A_OFF, sB = base + Cfg::B_OFF;
+    const uint32_t bar0 = base + Cfg::BAR_OFF;
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
+    auto rfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 4 + a); };
+    auto rempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 6 + a); };
+    int32_t* rs_buf = reinterpret_cast<int32_t*>(smem + Cfg::RS_OFF);
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + Cfg::TMEMPTR_OFF);
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_a);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(full_bar(s), 1);
+            ptx::mbar_init(empty_bar(s), CN * (1 + (RS ? 4 : 0)));
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull_bar(a), 1);
+            ptx::mbar_init(tempty_bar(a), 4);
+            ptx::mbar_init(rfull_bar(a), 4);
+            ptx::mbar_init(rempty_bar(a), 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<Cfg::TMEM_COLS>(ptx::smem_u32(tmem_ptr));
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (CN > 1) ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_ptr;
+
+    const int num_clusters = gridDim.x / CN;
+    const int cluster_id = blockIdx.x / CN;
+    const int total = p.num_m_tiles * p.num_n_groups;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t pol_b = ptx::policy_evict_last();  // weights are re-read by every M tile
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < total; t += num_clusters) {
+                const int m_blk = t / p.num_n_groups, ng = t % p.num_n_groups;
+                const int m0 = m_blk * BM;
+                const int n0 = (ng * CN + (int)rank) * BN;
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(full_bar(stage), A_STAGE_BYTES + Cfg::B_STAGE_BYTES);
+                    const uint32_t a_dst = sA + stage * A_STAGE_BYTES;
+                    if (CN == 1) {
+                        ptx::tma_load_2d(a_dst, &tmap_a, kb * kKBlock, m0, full_bar(stage));
+                    } else {
+                        constexpr int SLICE = BM / CN;
+                        ptx::tma_load_2d_mc(a_dst + rank * SLICE * kKBlock, &tmap_a, kb * kKBlock,
+                                            m0 + (int)rank * SLICE, full_bar(stage),
+                                            (uint16_t)((1u << CN) - 1));
+                    }
+                    const int8_t* src = p.pb + ((size_t)kb * p.np + n0) * kKBlock;
+                    ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE_BYTES, src, Cfg::B_STAGE_BYTES,
+                                        full_bar(stage), pol_b);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_u8s8_s32<BM, BN>();
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cluster_id; t < total; t += num_clusters) {
+                ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    ptx::mbar_wait(full_bar(stage), phase);
+                    ptx::tc_fence_after();
+                    const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE_BYTES);
+                    const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE_BYTES);
+#pragma unroll
+                    for (int ks = 0; ks < kKBlock / 32; ++ks)
+                        ptx::mma_i8(d, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb | ks) != 0);
+                    if (CN == 1)
+                        ptx::tc_commit(empty_bar(stage));
+                    else
+                        ptx::tc_commit_mc(empty_bar(stage), (uint16_t)((1u << CN) - 1));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::tc_commit(tfull_bar(acc));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ epilogue
+        const int ew = warp - 4;  // == warp % 4: TMEM lanes [32*ew, 32*ew+32)
+        const int r = ew * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cluster_id; t < total; t += num_clusters) {
+            const int m_blk = t / p.num_n_groups, ng = t % p.num_n_groups;
+            const int m0 = m_blk * BM;
+            const int n0 = (ng * CN + (int)rank) * BN;
+            ptx::mbar_wait(tfull_bar(acc), acc_phase);
+            ptx::tc_fence_after();
+            int32_t rowsum = 0;
+            if (RS) {
+                ptx::mbar_wait(rfull_bar(acc), acc_phase);
+                rowsum = rs_buf[acc * BM + r];
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(rempty_bar(acc));
+            }
+            const int row = m0 + r;
+            const bool valid = row < p.rows;
+#pragma unroll 1
+            for (int ch = 0; ch < BN / EPI_COLS; ++ch) {
+                uint32_t v[EPI_COLS];
+                const uint32_t taddr =
+                    tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + ch * EPI_COLS);
+                ptx::tmem_ld_32x32b_x16(taddr, v);
+                ptx::tmem_ld_wait();
+                const int col0 = n0 + ch * EPI_COLS;
+                if (valid && col0 < p.n) store_chunk<MODE>(p, row, col0, v, rowsum);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (RS && warp >= 8) {
+        // ------------------------------------------------ row sums of A
+        const int r = (warp - 8) * 32 + lane;
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cluster_id; t < total; t += num_clusters) {
+            ptx::mbar_wait(rempty_bar(acc), acc_phase ^ 1);
+            uint32_t sum = 0;
+            for (int kb = 0; kb < p.nkb; ++kb) {
+                ptx::mbar_wait(full_bar(stage), phase);
+                // the row's 8 16-byte chunks in rotated order: conflict-free
+                // across the warp; the sum is swizzle-invariant
+                const uint8_t* rowp = smem + Cfg::A_OFF + stage * A_STAGE_BYTES + r * kKBlock;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(rowp + ((q + r) & 7) * 16);
+                    sum = ptx::dp4a_uu(w.x, 0x01010101u, sum);
+                    sum = ptx::dp4a_uu(w.y, 0x01010101u, sum);
+                    sum = ptx::dp4a_uu(w.z, 0x01010101u, sum);
+                    sum = ptx::dp4a_uu(w.w, 0x01010101u, sum);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    if (CN == 1) {
+                        ptx::mbar_arrive(empty_bar(stage));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < CN; ++q) ptx::mbar_arrive_cluster(empty_bar(stage), q);
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            rs_buf[acc * BM + r] = (int32_t)sum;
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(rfull_bar(acc));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (CN > 1) ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// A (rows x k, row-major, lda) as a 2-D u8 tensor, box = 128 bytes x box_rows,
+// SWIZZLE_128B; out-of-range rows / k read as zero.
+bool make_tmap_a(CUtensorMap* m, const uint8_t* a, int rows, int k, int lda, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)lda};
+    cuuint32_t box[2] = {(cuuint32_t)kKBlock, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// small cache of encoded tensor maps keyed on the A view
+struct TmapKey {
+    const void* a;
+    int rows, k, lda, box;
+    bool operator==(const TmapKey& o) const {
+        return a == o.a && rows == o.rows && k == o.k && lda == o.lda && box == o.box;
+    }
+};
+struct TmapKeyHash {
+    size_t operator()(const TmapKey& t) const {
+        return std::hash<const void*>()(t.a) ^ ((size_t)t.rows * 1315423911u) ^ ((size_t)t.k << 20) ^
+               ((size_t)t.lda << 40) ^ (size_t)t.box;
+    }
+};
+
+bool cached_tmap_a(CUtensorMap* out, const uint8_t* a, int rows, int k, int lda, int box_rows) {
+    static std::mutex mu;
+    static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
+    TmapKey key{a, rows, k, lda, box_rows};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
+    if (!make_tmap_a(out, a, rows, k, lda, box_rows)) return false;
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(key, *out);
+    return true;
+}
+
+template <int BN, int CN, int STAGES, int MODE, bool RS>
+cudaError_t launch_variant(const GemmArgs& g, cudaStream_t s) {
+    using Cfg = TcCfg<BN, CN, STAGES>;
+    auto kern = gemm_tc_kernel<BN, CN, STAGES, MODE, RS>;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = true;
+    }
+    CUtensorMap tmap;
+    if (!cached_tmap_a(&tmap, g.a, g.rows, g.k, g.lda, BM / CN)) return cudaErrorInvalidValue;
+    TcParams p;
+    p.pb = g.pb->data;
+    p.np = g.pb->np;
+    p.nkb = g.pb->kp / kKBlock;
+    p.n = g.pb->n;
+    p.rows = g.rows;
+    p.num_m_tiles = ceil_div_i(g.rows, BM);
+    p.num_n_groups = g.pb->np / (BN * CN);
+    p.rec = g.ep ? g.ep->rec : nullptr;
+    p.zp_c = g.ep ? g.ep->zp_c : 0;
+    p.relu = g.ep ? g.ep->relu : 0;
+    p.bias_add = g.bias_add;
+    p.c = g.c;
+    p.ldc = g.ldc;
+    const int total = p.num_m_tiles * p.num_n_groups;
+    const int max_clusters = sm_count(dev) / CN;
+    const int clusters = total < max_clusters ? total : max_clusters;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CN);
+    cfg.blockDim = dim3(RS ? 384 : 256);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CN;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, p);
+    count_launch();
+    return e;
+}
+
+template <int BN, int CN, int STAGES>
+cudaError_t launch_modes(const GemmArgs& g, cudaStream_t s) {
+    if (g.raw) return launch_variant<BN, CN, STAGES, 0, false>(g, s);
+    const bool rs = g.ep->need_rowsum;
+    if (g.ep->rounding == Q8G_ROUND_F32_RNE)
+        return rs ? launch_variant<BN, CN, STAGES, 1, true>(g, s) : launch_variant<BN, CN, STAGES, 1, false>(g, s);
+    return rs ? launch_variant<BN, CN, STAGES, 2, true>(g, s) : launch_variant<BN, CN, STAGES, 2, false>(g, s);
+}
+
+}  // namespace
+
+bool tc_supported(const GemmArgs& g) {
+    return get_encode() != nullptr && (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) && (g.lda % 16 == 0) &&
+           g.k % 16 == 0 && g.k >= 16;
+}
+
+cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
+    if (tile_kind == kSmallM) return launch_modes<32, 8, 10>(g, s);
+    return launch_modes<256, 1, 4>(g, s);
+}
+
+}  // namespace q8g

@@ -1,0 +1,170 @@
+// q8g_internal.cuh — shared internals of the B200 q8gemm library.
+//
+// Data layout in HBM:
+//   packed B  : K padded to KP = round_up(K,128), N padded to NP =
+//               round_up(N,256).  For k-block kb (128 bytes of K) and output
+//               channel n, the 128 K-bytes of (kb, n) live at
+//               ((kb * NP) + n) * 128, with 16-byte chunk ch stored at chunk
+//               slot ch ^ (n & 7).  Every 8 channels form one 1024-byte
+//               SWIZZLE_128B atom, so any tile of BN (multiple of 8) channels
+//               of one k-block is a contiguous, pre-swizzled BN*128-byte run
+//               that one cp.async.bulk drops into shared memory in exactly
+//               the canonical tcgen05 K-major SW128 layout.
+//   epilogue  : one 16-byte record per (padded) output column:
+//               {int32 c, int32 zp_b, fp32 mult | fp64 mult}.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/q8g_b200.h"
+
+namespace q8g {
+
+constexpr int kKBlock = 128;  // bytes of K per pipeline stage / pack block
+constexpr int kNPad = 256;    // output-channel padding of packed B
+
+inline int round_up_i(int v, int m) { return ((v + m - 1) / m) * m; }
+inline int ceil_div_i(int v, int d) { return (v + d - 1) / d; }
+
+// ---- error plumbing ----
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define Q8G_CUDA_TRY(expr)                                   \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return ::q8g::cuda_fail(_e, #expr); \
+    } while (0)
+
+// RAII device guard
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct EpiRecord {  // 16 bytes, one per padded output column
+    int32_t c;      // bias + bias_add - zp_a*colsum + K*zp_a*zp_b (mod 2^32)
+    int32_t zpb;    // weight zero point of this column
+    union {
+        float mf;   // F32_RNE multiplier
+        double md;  // REF multiplier (occupies bytes 8..15)
+    };
+};
+static_assert(sizeof(EpiRecord) == 16, "EpiRecord must be 16 bytes");
+
+}  // namespace q8g
+
+struct q8g_packed_b {
+    int device = 0;
+    int k = 0, n = 0;   // logical K x N
+    int kp = 0, np = 0; // padded
+    int max_abs = 0;
+    q8g_blocking blocking{};
+    int8_t* data = nullptr;       // device, kp*np bytes
+    int32_t* colsum_dev = nullptr; // device, np entries (zero beyond n)
+    int32_t* colsum_host = nullptr;
+};
+
+struct q8g_epilogue {
+    int device = 0;
+    int n = 0, np = 0;
+    int k_total = 0;
+    int32_t zp_a = 0, zp_c = 0;
+    int rounding = Q8G_ROUND_REF;
+    int relu = 0;
+    bool need_rowsum = false;  // any zp_b[j] != 0 (pipeline.hpp:114-119)
+    q8g::EpiRecord* rec = nullptr;  // device, np records
+};
+
+struct q8g_dw_filter {
+    int device = 0;
+    int c = 0;
+    int32_t zp_a = 0, zp_c = 0;
+    int relu = 0;
+    int8_t* w = nullptr;             // device [9][c]
+    q8g::EpiRecord* rec = nullptr;   // device, c records (fp32 mult)
+};
+
+namespace q8g {
+
+// Tile kinds chosen by the dispatch cache (dispatch.hpp:248 TileKind analog)
+enum TileKind : int { kGeneric = 0, kSmallM = 1, kLargeM = 2 };
+
+struct ShapeKey {
+    int m_class, n_class, k_class, align;
+    bool operator==(const ShapeKey& o) const {
+        return m_class == o.m_class && n_class == o.n_class && k_class == o.k_class &&
+               align == o.align;
+    }
+};
+struct ShapeKeyHash {
+    size_t operator()(const ShapeKey& s) const {
+        return ((size_t)s.m_class * 131 + s.n_class) * 131 * 131 + s.k_class * 131 + s.align;
+    }
+};
+
+}  // namespace q8g
+
+struct q8g_kernel_cache {
+    bool generic_only = false;
+    std::mutex mu;
+    std::unordered_map<q8g::ShapeKey, int, q8g::ShapeKeyHash> table;
+    uint64_t builds = 0;
+};
+
+namespace q8g {
+
+// ---- kernels (launchers return cudaError_t of the launch) ----
+cudaError_t launch_pack_b(const int8_t* b, int k, int n, int ldb, int8_t* packed, int kp, int np,
+                          int32_t* colsum, int* max_abs, cudaStream_t s);
+cudaError_t launch_unpack_b(const int8_t* packed, int k, int n, int kp, int np, int8_t* out,
+                            int ldb, cudaStream_t s);
+
+struct GemmArgs {
+    const uint8_t* a;   // points at row 0 of the stripe
+    int rows;           // rows in the stripe
+    int k, lda;
+    const q8g_packed_b* pb;
+    const q8g_epilogue* ep;  // null for raw
+    const int32_t* bias_add; // raw writer only, may be null
+    void* c;            // points at row 0 of the stripe
+    int ldc;
+    bool raw;
+};
+cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
+cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s);
+bool tc_supported(const GemmArgs& g);
+
+struct ConvArgs {
+    const uint8_t* x;  // first image of the shard
+    int nb, h, w, c;
+    int32_t zp_a;
+    const q8g_packed_b* pw;
+    const q8g_epilogue* ep;  // null for raw
+    void* y;
+    bool raw;
+};
+cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s);
+
+cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c,
+                             const q8g_dw_filter* f, uint8_t* y, cudaStream_t s);
+
+int sm_count(int device);
+
+}  // namespace q8g

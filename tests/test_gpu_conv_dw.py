@@ -1,0 +1,99 @@
+"""Parity of the conv3x3 (implicit GEMM) and depthwise-3x3 CUDA paths against
+the oracle (SURVEY.md App. A D2/D3 semantics; no reference symbol exists, so
+these are checked against the restated im2col -> reference-pinned GEMM ->
+requant pipeline and the restated depthwise loop)."""
+import numpy as np
+import pytest
+import torch
+
+import configs
+import paper_2101_05615_b200 as q8
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def conv_pipeline(cc: configs.ConvCase, c: int):
+    rp = q8.RequantParams(multiplier=1.0, zp_a=cc.zp_a, zp_c=cc.zp_c, k_total=9 * c, bias=cc.bias,
+                          zp_b_per_channel=cc.zp_b, multiplier_f32_per_channel=cc.mult_f32,
+                          rounding=q8.ROUND_F32_RNE)
+    return q8.OutputPipeline(([q8.ReluQuantized()] if cc.relu else []) + [q8.Requantize(rp)])
+
+
+def conv_oracle(orc, cc: configs.ConvCase):
+    nb, h, w, c = cc.x.shape
+    cols = orc.im2col3x3(cc.x, cc.zp_a)
+    wt = cc.w.reshape(9 * c, -1)
+    acc = orc.naive_gemm_i32(cols, wt)
+    out = orc.requant_matrix(acc, orc.row_offsets(cols), orc.col_offsets(wt), cc.zp_a, cc.zp_b, 9 * c, cc.bias, 1,
+                             cc.mult_f32, cc.zp_c, cc.relu, per_channel=True)
+    return acc, out
+
+
+@pytest.mark.parametrize("shape", [(1, 5, 7, 4, 8), (2, 9, 9, 16, 24), (3, 14, 14, 64, 64), (1, 3, 3, 3, 5)])
+def test_conv3x3_small_vs_oracle(cuda, orc, shape):
+    nb, h, w, c, oc = shape
+    cc = configs.conv_case(orc, nb, h, w, c, oc, seed=sum(shape))
+    pw = q8.prepack_conv3x3_weights(cc.w)
+    acc, exp = conv_oracle(orc, cc)
+    y = torch.zeros((nb, h, w, oc), dtype=torch.uint8, device="cuda")
+    q8.execute_conv3x3(dev(cc.x), pw, y, conv_pipeline(cc, c))
+    torch.cuda.synchronize()
+    assert (y.cpu().numpy().reshape(-1, oc) == exp).all()
+    yr = torch.zeros((nb, h, w, oc), dtype=torch.int32, device="cuda")
+    q8.execute_conv3x3(dev(cc.x), pw, yr, q8.OutputPipeline([q8.WriteRawI32()]), zp_a=cc.zp_a)
+    torch.cuda.synchronize()
+    assert (yr.cpu().numpy().reshape(-1, oc) == acc).all()
+
+
+def test_conv3x3_c3_full_vs_oracle(cuda, orc):
+    cc = configs.conv_case(orc)  # 32x56x56x64 -> 64, BASELINE configs[3]
+    pw = q8.prepack_conv3x3_weights(cc.w)
+    _, exp = conv_oracle(orc, cc)
+    y = torch.zeros((32, 56, 56, 64), dtype=torch.uint8, device="cuda")
+    q8.execute_conv3x3(dev(cc.x), pw, y, conv_pipeline(cc, 64))
+    torch.cuda.synchronize()
+    assert (y.cpu().numpy().reshape(-1, 64) == exp).all()
+    # batch shards (one per GPU at 1/2/4/8) compose to the same output
+    y2 = torch.zeros_like(y)
+    for i0, i1 in [(0, 8), (8, 16), (16, 24), (24, 32)]:
+        q8.execute_conv3x3(dev(cc.x), pw, y2, conv_pipeline(cc, 64), image_begin=i0, image_end=i1)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+
+
+def dw_filter(dc: configs.DwCase):
+    rp = q8.RequantParams(multiplier=1.0, zp_a=dc.zp_a, zp_c=dc.zp_c, k_total=9, bias=dc.bias,
+                          zp_b_per_channel=dc.zp_w, multiplier_f32_per_channel=dc.mult_f32,
+                          rounding=q8.ROUND_F32_RNE)
+    return q8.DepthwiseFilter(dc.w, rp, relu=dc.relu)
+
+
+@pytest.mark.parametrize("shape", [(1, 4, 5, 4), (2, 7, 9, 12), (1, 16, 16, 256), (2, 3, 3, 7), (1, 1, 1, 8)])
+def test_dwconv_small_vs_oracle(cuda, orc, shape):
+    nb, h, w, c = shape
+    dc = configs.dw_case(orc, nb, h, w, c, seed=sum(shape))
+    exp, _ = orc.dwconv3x3(dc.x, dc.zp_a, dc.w, dc.zp_w, dc.bias, dc.mult_f32, dc.zp_c, dc.relu)
+    y = torch.zeros(shape, dtype=torch.uint8, device="cuda")
+    q8.execute_dwconv3x3(dev(dc.x), dw_filter(dc), y)
+    torch.cuda.synchronize()
+    assert (y.cpu().numpy() == exp).all()
+
+
+def test_dwconv_c4_full_vs_oracle(cuda, orc):
+    dc = configs.dw_case(orc)  # 32x112x112x256, BASELINE configs[4]
+    exp, _ = orc.dwconv3x3(dc.x, dc.zp_a, dc.w, dc.zp_w, dc.bias, dc.mult_f32, dc.zp_c, dc.relu)
+    f = dw_filter(dc)
+    y = torch.zeros(dc.x.shape, dtype=torch.uint8, device="cuda")
+    xd = dev(dc.x)
+    q8.execute_dwconv3x3(xd, f, y)
+    torch.cuda.synchronize()
+    assert (y.cpu().numpy() == exp).all()
+    y2 = torch.zeros_like(y)
+    for i0, i1 in [(0, 3), (3, 17), (17, 32)]:
+        q8.execute_dwconv3x3(xd, f, y2, image_begin=i0, image_end=i1)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)

@@ -1,0 +1,321 @@
+"""Parity of the CUDA GEMM path (through the C ABI) against the pinned oracle
+and the reference's golden fixtures.  Bit-exact: int32 accumulators and u8
+outputs.  Mirrors proj/tests/test_engine.cpp and acceptance.cpp criteria 1,
+5, 6, 8."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import configs
+import paper_2101_05615_b200 as q8
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_raw(a, pw, cache=None, threads=1):
+    m = a.shape[0]
+    out = torch.full((m, pw.n_total), -1, dtype=torch.int32, device="cuda")
+    ad = dev(a) if isinstance(a, np.ndarray) else a
+    for t in range(threads):
+        q8.execute_gemm(ad, pw, out, q8.OutputPipeline([q8.WriteRawI32()]), thread_id=t, num_threads=threads,
+                        cache=cache)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def requant_pipeline(c: configs.GemmCase, k: int, rounding: int):
+    rp = q8.RequantParams(multiplier=float(c.mult_f64) if not c.per_channel else 1.0, zp_a=c.zp_a,
+                          zp_b=int(c.zp_b) if not c.per_channel else 0, zp_c=c.zp_c, k_total=k, bias=c.bias,
+                          rounding=rounding)
+    if c.per_channel:
+        rp.zp_b_per_channel = c.zp_b
+        rp.multiplier_f32_per_channel = c.mult_f32
+    elif rounding == q8.ROUND_F32_RNE:
+        rp.multiplier_f32_per_channel = np.full(c.b.shape[1], np.float32(c.mult_f64))
+    stages = ([q8.ReluQuantized()] if c.relu else []) + [q8.Requantize(rp)]
+    return q8.OutputPipeline(stages)
+
+
+def oracle_requant(orc, c: configs.GemmCase, acc, rounding):
+    mult = c.mult_f32 if c.per_channel else (c.mult_f64 if rounding == 0 else np.float32(c.mult_f64))
+    return orc.requant_matrix(acc, orc.row_offsets(c.a), orc.col_offsets(c.b), c.zp_a, c.zp_b, c.a.shape[1],
+                              c.bias, rounding, mult, c.zp_c, c.relu, per_channel=c.per_channel)
+
+
+# ------------------------------------------------------------------ packing
+
+def test_pack_roundtrip_colsums_maxabs(cuda, orc):
+    r = orc.rng(41)
+    for k, n in [(100, 37), (1, 1), (128, 256), (129, 257), (4096, 64), (320, 800), (7, 1000)]:
+        b = r.i8_matrix(k, n)
+        pw = q8.prepack_weights(b)
+        assert (pw.unpack() == b).all()
+        assert (pw.col_offsets == orc.col_offsets(b)).all()
+        assert pw.max_abs == int(np.abs(b.astype(np.int32)).max())
+    z = q8.prepack_weights(np.zeros((10, 6), np.int8))
+    assert (z.col_offsets == 0).all() and z.max_abs == 0
+
+
+def test_pack_from_device_tensor(cuda, orc):
+    b = orc.rng(3).i8_matrix(300, 70)
+    pw = q8.prepack_weights(dev(b))
+    assert (pw.unpack() == b).all()
+
+
+# ------------------------------------------------------------------ raw int32 parity
+
+def test_gemm_1x1x1(cuda):
+    pw = q8.prepack_weights(np.array([[3]], np.int8))
+    assert run_raw(np.array([[2]], np.uint8), pw)[0, 0] == 6
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_raw_small_shape_sweep(cuda, orc, generic):
+    # acceptance.cpp criterion 1 (sampled exhaustive grid)
+    cache = q8.KernelCache(generic_only=generic)
+    r = orc.rng(1001)
+    dims = [1, 2, 3, 7, 8, 15, 16, 17, 33]
+    for m in dims:
+        for n in dims:
+            for k in [1, 5, 16, 32, 48]:
+                a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+                got = run_raw(a, q8.prepack_weights(b), cache=cache)
+                assert (got == orc.naive_gemm_i32(a, b)).all(), (m, n, k)
+
+
+def test_raw_random_shapes_threads(cuda, orc):
+    # test_engine.cpp:87-113: shapes x workers
+    r = orc.rng(113)
+    for trial in range(40):
+        m, n, k = r.int(1, 300), r.int(1, 300), r.int(1, 300)
+        if trial % 2:
+            k = 16 * r.int(1, 20)  # tensor-core eligible
+        a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+        pw = q8.prepack_weights(b)
+        exp = orc.naive_gemm_i32(a, b)
+        for threads in (1, 3):
+            assert (run_raw(a, pw, threads=threads) == exp).all(), (m, n, k, threads)
+
+
+@pytest.mark.parametrize("m", [1, 64, 128, 129, 200, 256, 300, 1000])
+@pytest.mark.parametrize("n,k", [(32, 128), (256, 256), (800, 320), (300, 144), (4096, 512)])
+def test_tensor_core_paths_raw(cuda, orc, m, n, k):
+    r = orc.rng(m * 7 + n * 3 + k)
+    a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+    pw = q8.prepack_weights(b)
+    kc = q8.KernelCache()
+    assert kc.tile(m, n, k, k) == (1 if m <= 128 else 2)
+    assert (run_raw(a, pw, cache=kc) == orc.naive_gemm_i32(a, b)).all()
+
+
+def test_specialised_equals_generic(cuda, orc):
+    # test_engine.cpp:291-311 / acceptance criterion 6
+    spec, gen = q8.KernelCache(False), q8.KernelCache(True)
+    r = orc.rng(163)
+    for m in (1, 5, 14, 28, 29, 40, 130, 257):
+        for n in (5, 32, 64, 70, 300):
+            k = 16 * r.int(1, 12)
+            a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+            pw = q8.prepack_weights(b)
+            assert (run_raw(a, pw, cache=spec) == run_raw(a, pw, cache=gen)).all()
+
+
+def test_wide_leading_dimensions(cuda, orc):
+    # test_engine.cpp:313-337: output window in a wider buffer; outside untouched
+    r = orc.rng(167)
+    for (m, n, k) in [(11, 23, 31), (150, 70, 64), (100, 300, 256)]:
+        a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+        pw = q8.prepack_weights(b)
+        back = torch.full((m + 2, n + 40), -99, dtype=torch.int32, device="cuda")
+        view = back[1:m + 1, 8:8 + n]
+        abig = torch.zeros((m, k + 32), dtype=torch.uint8, device="cuda")
+        abig[:, :k] = dev(a)
+        q8.execute_gemm(abig[:, :k], pw, view, q8.OutputPipeline([q8.WriteRawI32()]))
+        torch.cuda.synchronize()
+        bk = back.cpu().numpy()
+        assert (bk[1:m + 1, 8:8 + n] == orc.naive_gemm_i32(a, b)).all()
+        assert (bk[0] == -99).all() and (bk[m + 1] == -99).all()
+        assert (bk[:, :8] == -99).all() and (bk[:, 8 + n:] == -99).all()
+
+
+def test_worker_calls_compose_in_any_order(cuda, orc):
+    # test_engine.cpp:115-139
+    r = orc.rng(127)
+    m, n, k = 700, 96, 128
+    a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+    pw = q8.prepack_weights(b)
+    serial = run_raw(a, pw)
+    for order in ([3, 1, 0, 2], [2, 3, 1, 0]):
+        out = torch.full((m, n), -7, dtype=torch.int32, device="cuda")
+        for t in order:
+            q8.execute_gemm(dev(a), pw, out, q8.OutputPipeline([q8.WriteRawI32()]), thread_id=t, num_threads=4)
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy() == serial).all()
+
+
+def test_host_views_reference_convention(cuda, orc):
+    r = orc.rng(5)
+    a, b = r.u8_matrix(77, 96), r.i8_matrix(96, 33)
+    pw = q8.prepack_weights(b)
+    out = np.full((77, 33), -1, np.int32)
+    q8.execute_gemm(a, pw, out, q8.OutputPipeline([q8.WriteRawI32()]))
+    assert (out == orc.naive_gemm_i32(a, b)).all()
+
+
+def test_bias_add_stage_raw(cuda, orc):
+    r = orc.rng(157)
+    a, b = r.u8_matrix(130, 64), r.i8_matrix(64, 40)
+    bias = r.ints(-2000, 2000, 40)
+    pw = q8.prepack_weights(b)
+    out = torch.zeros((130, 40), dtype=torch.int32, device="cuda")
+    q8.execute_gemm(dev(a), pw, out, q8.OutputPipeline([q8.BiasAdd(bias), q8.WriteRawI32()]))
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == orc.naive_gemm_i32(a, b) + bias).all()
+
+
+# ------------------------------------------------------------------ requant parity
+
+def test_c0_ref_mode_bit_exact_vs_reference_fixture(cuda, orc):
+    g = np.load(GOLD / "c0_reference.npz")
+    c = configs.gemm_case(orc, "C0", *configs.CONFIG_SHAPES["C0"])
+    pw = q8.prepack_weights(c.b)
+    assert (pw.col_offsets == g["col_offsets"]).all()
+    for relu, key in ((False, "out"), (True, "out_relu")):
+        c.relu = relu
+        for generic in (False, True):
+            out = torch.zeros((64, 800), dtype=torch.uint8, device="cuda")
+            q8.execute_gemm(dev(c.a), pw, out, requant_pipeline(c, 320, q8.ROUND_REF),
+                            cache=q8.KernelCache(generic))
+            torch.cuda.synchronize()
+            assert (out.cpu().numpy() == g[key]).all(), (relu, generic)
+
+
+def test_c0_f32_mode_vs_oracle(cuda, orc):
+    c = configs.gemm_case(orc, "C0", *configs.CONFIG_SHAPES["C0"])
+    pw = q8.prepack_weights(c.b)
+    out = torch.zeros((64, 800), dtype=torch.uint8, device="cuda")
+    q8.execute_gemm(dev(c.a), pw, out, requant_pipeline(c, 320, q8.ROUND_F32_RNE))
+    torch.cuda.synchronize()
+    exp = oracle_requant(orc, c, orc.naive_gemm_i32(c.a, c.b), 1)
+    assert (out.cpu().numpy() == exp).all()
+
+
+def test_ref_small_fixture_requant(cuda):
+    g = np.load(GOLD / "ref_small.npz")
+    for i in range(int(g["count"])):
+        a, b = g[f"{i}_a"], g[f"{i}_b"]
+        rp = q8.RequantParams(multiplier=float(g[f"{i}_mult"]), zp_a=int(g[f"{i}_zp_a"]), zp_b=int(g[f"{i}_zp_b"]),
+                              zp_c=int(g[f"{i}_zp_c"]), k_total=a.shape[1], bias=g[f"{i}_bias"])
+        stages = ([q8.ReluQuantized()] if bool(g[f"{i}_relu"]) else []) + [q8.Requantize(rp)]
+        pw = q8.prepack_weights(b)
+        out = np.zeros((a.shape[0], b.shape[1]), np.uint8)
+        q8.execute_gemm(a, pw, out, q8.OutputPipeline(stages))
+        assert (out == g[f"{i}_out"]).all(), i
+        acc = np.zeros((a.shape[0], b.shape[1]), np.int32)
+        q8.execute_gemm(a, pw, acc, q8.OutputPipeline([q8.WriteRawI32()]))
+        assert (acc == g[f"{i}_acc"]).all(), i
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 4096, 4096), (100, 1000, 640), (300, 512, 1024), (1, 256, 4096)])
+def test_per_channel_f32_requant_vs_oracle(cuda, orc, m, n, k):
+    # C1 semantics (per-channel zp_b / alpha_B, bias, ReLU, F32_RNE)
+    c = configs.gemm_case(orc, "C1", m, n, k, seed=m + n + k)
+    pw = q8.prepack_weights(c.b)
+    acc = orc.naive_gemm_i32(c.a, c.b)
+    assert (run_raw(c.a, pw) == acc).all()
+    exp = oracle_requant(orc, c, acc, 1)
+    for generic in (False, True):
+        out = torch.zeros((m, n), dtype=torch.uint8, device="cuda")
+        q8.execute_gemm(dev(c.a), pw, out, requant_pipeline(c, k, q8.ROUND_F32_RNE), cache=q8.KernelCache(generic))
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy() == exp).all(), generic
+    sat = np.mean((exp == 255) | (exp == c.zp_c))
+    assert sat < 0.8  # outputs are spread, not all clamped
+
+
+def test_relu_is_max_with_zp_c(cuda, orc):
+    # test_engine.cpp:235-259
+    c = configs.gemm_case(orc, "C1", 200, 96, 256, seed=149)
+    pw = q8.prepack_weights(c.b)
+    outs = []
+    for relu in (False, True):
+        c.relu = relu
+        o = torch.zeros((200, 96), dtype=torch.uint8, device="cuda")
+        q8.execute_gemm(dev(c.a), pw, o, requant_pipeline(c, 256, q8.ROUND_F32_RNE))
+        outs.append(o.cpu().numpy())
+    assert (outs[1] == np.maximum(outs[0], c.zp_c)).all()
+
+
+def test_bias_add_stage_equals_params_bias(cuda, orc):
+    # test_engine.cpp:261-289
+    r = orc.rng(157)
+    a, b = r.u8_matrix(13, 64), r.i8_matrix(64, 17)
+    bias = r.ints(-2000, 2000, 17)
+    pw = q8.prepack_weights(b)
+    rp = dict(multiplier=0.0015, zp_a=4, zp_b=-9, zp_c=31, k_total=64)
+    o1 = np.zeros((13, 17), np.uint8)
+    o2 = np.ones((13, 17), np.uint8)
+    q8.execute_gemm(a, pw, o1, q8.OutputPipeline([q8.Requantize(q8.RequantParams(**rp, bias=bias))]))
+    q8.execute_gemm(a, pw, o2, q8.OutputPipeline([q8.BiasAdd(bias), q8.Requantize(q8.RequantParams(**rp))]))
+    assert (o1 == o2).all()
+
+
+def test_zero_zp_b_skips_row_sums_same_result(cuda, orc):
+    r = orc.rng(11)
+    a, b = r.u8_matrix(256, 256), r.i8_matrix(256, 256)
+    pw = q8.prepack_weights(b)
+    rp = q8.RequantParams(multiplier=0.0003, zp_a=128, zp_b=0, zp_c=10, k_total=256, rounding=q8.ROUND_F32_RNE,
+                          multiplier_f32_per_channel=np.full(256, 0.0003, np.float32))
+    out = np.zeros((256, 256), np.uint8)
+    q8.execute_gemm(a, pw, out, q8.OutputPipeline([q8.Requantize(rp)]))
+    acc = orc.naive_gemm_i32(a, b)
+    exp = orc.requant_matrix(acc, None, orc.col_offsets(b), 128, 0, 256, None, 1, np.float32(0.0003), 10, False,
+                             per_channel=False)
+    assert (out == exp).all()
+
+
+# ------------------------------------------------------------------ errors
+
+def test_argument_validation(cuda):
+    a = np.ones((4, 6), np.uint8)
+    pw = q8.prepack_weights(np.ones((6, 5), np.int8))
+    raw = q8.OutputPipeline([q8.WriteRawI32()])
+    with pytest.raises(q8.InvalidArgument, match="A columns must equal the packed weight K"):
+        q8.execute_gemm(np.ones((4, 7), np.uint8), pw, np.zeros((4, 5), np.int32), raw)
+    with pytest.raises(q8.InvalidArgument, match="output must be M x N"):
+        q8.execute_gemm(a, pw, np.zeros((4, 4), np.int32), raw)
+    with pytest.raises(q8.InvalidArgument, match="thread_id"):
+        q8.execute_gemm(a, pw, np.zeros((4, 5), np.int32), raw, thread_id=1, num_threads=1)
+    with pytest.raises(q8.InvalidArgument, match="thread_id"):
+        q8.execute_gemm(a, pw, np.zeros((4, 5), np.int32), raw, thread_id=0, num_threads=0)
+    with pytest.raises(q8.InvalidArgument, match="writer does not match"):
+        q8.execute_gemm(a, pw, np.zeros((4, 5), np.uint8), raw)
+    big = q8.prepack_weights(np.full((64, 2), 127, np.int8))
+    with pytest.raises(q8.InvalidArgument, match="split outliers"):
+        q8.execute_gemm(np.full((2, 64), 255, np.uint8), big, np.zeros((2, 2), np.int32), raw,
+                        variant=q8.KernelVariant.kAccI16)
+    q8.execute_gemm(np.full((2, 64), 255, np.uint8), big, np.zeros((2, 2), np.int32), raw)
+
+
+def test_i16_variant_runs_exact_path(cuda, orc):
+    # test_engine.cpp:141-159: accepted when the static bound holds, same result
+    r = orc.rng(131)
+    a = r.u8_matrix(30, 80)
+    b = np.array([[r.int(-4, 4) for _ in range(20)] for _ in range(80)], np.int8)
+    pw = q8.prepack_weights(b, q8.select_blocking(30, 20, 80, q8.BlockingParams(kcb=32)))
+    out = np.zeros((30, 20), np.int32)
+    q8.execute_gemm(a, pw, out, q8.OutputPipeline([q8.WriteRawI32()]), variant=q8.KernelVariant.kAccI16)
+    assert (out == orc.naive_gemm_i32(a, b)).all()
+
+
+def test_launch_counter_moves(cuda, orc):
+    before = q8.launch_count()
+    run_raw(np.ones((4, 16), np.uint8), q8.prepack_weights(np.ones((16, 4), np.int8)))
+    assert q8.launch_count() > before
