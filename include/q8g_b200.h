@@ -62,6 +62,13 @@ const char* q8g_last_error(void);
 int q8g_version(void);
 /* number of CUDA kernels this library has launched in this process */
 uint64_t q8g_launch_count(void);
+/* per kernel family: [0] pack, [1] GEMM CUDA-core, [2] GEMM tcgen05 small-M,
+ * [3] GEMM tcgen05 large-M, [4] conv CUDA-core, [5] conv tcgen05,
+ * [6] depthwise CUDA-core, [7] depthwise tcgen05 */
+int q8g_launch_stats(uint64_t* counts, int n);
+/* debug (env Q8G_TC_TRACE set): 8 globaltimer stamps per CTA of the last
+ * tensor-core GEMM launch; returns the number of CTA records copied */
+int q8g_debug_tc_trace(uint64_t* out, int max_ctas);
 
 /* ---- blocking (dispatch.hpp:17-30, pack.hpp:24-37) ---- */
 int q8g_blocking_defaults(q8g_blocking* out);

@@ -25,4 +25,4 @@ from .api import (  # noqa: F401
     prepack_weights,
     select_blocking,
 )
-from ._lib import InvalidArgument, Q8GError, launch_count  # noqa: F401
+from ._lib import InvalidArgument, Q8GError, launch_count, launch_stats  # noqa: F401

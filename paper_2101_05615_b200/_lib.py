@@ -54,6 +54,8 @@ _SIGS = [
     ("q8g_last_error", C.c_char_p, []),
     ("q8g_version", _I, []),
     ("q8g_launch_count", C.c_uint64, []),
+    ("q8g_launch_stats", _I, [C.POINTER(C.c_uint64), _I]),
+    ("q8g_debug_tc_trace", _I, [C.POINTER(C.c_uint64), _I]),
     ("q8g_blocking_defaults", _I, [C.POINTER(Blocking)]),
     ("q8g_blocking_validate", _I, [C.POINTER(Blocking)]),
     ("q8g_select_blocking", _I, [_I, _I, _I, C.POINTER(Blocking), C.POINTER(Blocking)]),
@@ -120,3 +122,14 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(load().q8g_launch_count())
+
+
+FAMILIES = ("pack", "gemm_simt", "gemm_tc_small_m", "gemm_tc_large_m", "conv_simt", "conv_tc", "dw_simt",
+            "dw_tc")
+
+
+def launch_stats() -> dict:
+    """Launch counts per kernel family (evidence of which kernel ran)."""
+    arr = (C.c_uint64 * len(FAMILIES))()
+    check(load().q8g_launch_stats(arr, len(FAMILIES)))
+    return {f: int(v) for f, v in zip(FAMILIES, arr)}

@@ -130,7 +130,6 @@ class PackedWeight:
         co = np.zeros(self.n_total, dtype=np.int32)
         check(load().q8g_packed_b_col_offsets(self._h, co.ctypes.data))
         self.col_offsets = co  # ColOffsets over full K (quant.hpp:31-34)
-        self._epilogues = {}
 
     @property
     def handle(self):
@@ -149,9 +148,6 @@ class PackedWeight:
 
     def close(self):
         if self._owner and self._h:
-            for ep in self._epilogues.values():
-                load().q8g_epilogue_free(ep)
-            self._epilogues.clear()
             load().q8g_free_packed_b(self._h)
             self._h = C.c_void_p()
 
@@ -300,12 +296,13 @@ class OutputPipeline:
                                     f"{type(s).__name__} is not on the B200 hot path (SURVEY.md §8(f) next)")
 
     def epilogue(self, pw: PackedWeight) -> C.c_void_p:
-        """Fold [BiasAdd]* [ReluQuantized] Requantize into the device table
-        (cached per packed weight; pipelines are immutable)."""
-        key = id(self)
-        ep = pw._epilogues.get(key)
-        if ep is not None:
-            return ep
+        """Fold [BiasAdd]* [ReluQuantized] Requantize into the device table.
+        Cached on this pipeline per packed weight (the pipeline holds a
+        reference to the weight, so the key cannot be recycled)."""
+        cache = self.__dict__.setdefault("_eps", {})
+        hit = cache.get(id(pw))
+        if hit is not None and hit[0] is pw:
+            return hit[1]
         self._unsupported()
         rq = self.stages[-1]
         assert isinstance(rq, Requantize)
@@ -339,8 +336,15 @@ class OutputPipeline:
         h = C.c_void_p()
         check(load().q8g_epilogue_create(pw.handle, C.byref(cp), None if ba is None else ba.ctypes.data,
                                          C.byref(h)))
-        pw._epilogues[key] = h
+        cache[id(pw)] = (pw, h)
         return h
+
+    def __del__(self):
+        try:
+            for _, h in self.__dict__.get("_eps", {}).values():
+                load().q8g_epilogue_free(h)
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- dispatch cache

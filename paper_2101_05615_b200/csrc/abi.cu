@@ -21,6 +21,7 @@ namespace q8g {
 namespace {
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_family[kFamCount];
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -32,7 +33,10 @@ int cuda_fail(cudaError_t e, const char* what) {
     g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
     return Q8G_ECUDA;
 }
-void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+void count_launch(int family) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (family >= 0 && family < kFamCount) g_family[family].fetch_add(1, std::memory_order_relaxed);
+}
 
 int sm_count(int device) {
     static int cache[64] = {0};
@@ -90,6 +94,17 @@ extern "C" {
 const char* q8g_last_error(void) { return g_last_error.c_str(); }
 int q8g_version(void) { return 1; }
 uint64_t q8g_launch_count(void) { return g_launches.load(); }
+
+int q8g_debug_tc_trace(uint64_t* out, int max_ctas) {
+    if (!out || max_ctas < 1) return 0;
+    return tc_trace_copy(reinterpret_cast<unsigned long long*>(out), max_ctas);
+}
+
+int q8g_launch_stats(uint64_t* counts, int n) {
+    if (!counts || n < 1) return fail(Q8G_EINVAL, "launch_stats: bad arguments");
+    for (int i = 0; i < n; ++i) counts[i] = i < kFamCount ? g_family[i].load() : 0;
+    return Q8G_OK;
+}
 
 int q8g_blocking_defaults(q8g_blocking* out) {
     if (!out) return fail(Q8G_EINVAL, "null output");
@@ -453,15 +468,36 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
     const int rows = row_end - row_begin;
     if (rows == 0) return Q8G_OK;
     DeviceGuard dg(pb->device);
-    uint8_t* d_a = nullptr;
-    OutT* d_c = nullptr;
     const int lda_d = round_up_i(k, 16), ldc_d = pb->n;
+    // grow-only per-device staging buffers; host-view calls are synchronous
+    // and serialised per device by this lock
+    struct Staging {
+        std::mutex mu;
+        void* a = nullptr;
+        void* c = nullptr;
+        size_t a_bytes = 0, c_bytes = 0;
+    };
+    static Staging staging[64];
+    Staging& st = staging[pb->device & 63];
+    std::lock_guard<std::mutex> lock(st.mu);
     cudaError_t e;
-    if ((e = cudaMalloc(&d_a, (size_t)rows * lda_d)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(A)");
-    if ((e = cudaMalloc(&d_c, sizeof(OutT) * (size_t)rows * ldc_d)) != cudaSuccess) {
-        cudaFree(d_a);
-        return cuda_fail(e, "cudaMalloc(C)");
+    const size_t need_a = (size_t)rows * lda_d, need_c = sizeof(OutT) * (size_t)rows * ldc_d;
+    if (st.a_bytes < need_a) {
+        if (st.a) cudaFree(st.a);
+        st.a = nullptr;
+        st.a_bytes = 0;
+        if ((e = cudaMalloc(&st.a, need_a)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(A staging)");
+        st.a_bytes = need_a;
     }
+    if (st.c_bytes < need_c) {
+        if (st.c) cudaFree(st.c);
+        st.c = nullptr;
+        st.c_bytes = 0;
+        if ((e = cudaMalloc(&st.c, need_c)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(C staging)");
+        st.c_bytes = need_c;
+    }
+    uint8_t* d_a = (uint8_t*)st.a;
+    OutT* d_c = (OutT*)st.c;
     int rc = Q8G_OK;
     e = cudaMemcpy2DAsync(d_a, lda_d, a_host + (size_t)row_begin * lda, lda, k, rows,
                           cudaMemcpyHostToDevice, s);
@@ -481,8 +517,6 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) rc = cuda_fail(e, "D2H C");
     }
-    cudaFree(d_a);
-    cudaFree(d_c);
     return rc;
 }
 

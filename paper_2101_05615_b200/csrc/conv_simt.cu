@@ -120,7 +120,7 @@ cudaError_t launch_conv3x3_simt(const ConvArgs& a, cudaStream_t s) {
         conv3x3_simt_kernel<2><<<grid, THREADS, 0, s>>>(a.x, a.nb, a.h, a.w, a.c, a.zp_a, pw->data, pw->n,
                                                         pw->np, pw->kp, a.ep->rec, a.ep->zp_c, a.ep->relu,
                                                         a.ep->need_rowsum, a.y);
-    count_launch();
+    count_launch(kFamConvSimt);
     return cudaGetLastError();
 }
 

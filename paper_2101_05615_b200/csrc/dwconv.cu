@@ -90,7 +90,7 @@ cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c, cons
         dw_simple_kernel<<<blocks, 256, 0, s>>>(x, nb, h, w, c, f->zp_a, f->w, f->rec, f->zp_c, f->relu, y);
     else
         dw_scalar_kernel<<<blocks, 256, 0, s>>>(x, nb, h, w, c, f->zp_a, f->w, f->rec, f->zp_c, f->relu, y);
-    count_launch();
+    count_launch(kFamDw);
     return cudaGetLastError();
 }
 

@@ -130,7 +130,7 @@ cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
                                                      g.ep->relu, g.ep->need_rowsum, nullptr, g.c,
                                                      g.ldc);
     }
-    count_launch();
+    count_launch(kFamGemmSimt);
     return cudaGetLastError();
 }
 

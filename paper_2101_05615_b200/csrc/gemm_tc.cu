@@ -25,8 +25,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 
 #include "ptx.cuh"
@@ -46,8 +48,8 @@ struct TcCfg {
     static constexpr int A_OFF = 0;
     static constexpr int B_OFF = STAGES * A_STAGE_BYTES;
     static constexpr int BAR_OFF = B_OFF + STAGES * B_STAGE_BYTES;
-    // barriers: full[S], empty[S], tfull[2], tempty[2], rfull[2], rempty[2]
-    static constexpr int NUM_BARS = 2 * STAGES + 8;
+    // barriers: full[S], empty[S], tfull[2], tempty[2], rfull[2], rempty[2], rsdone[S]
+    static constexpr int NUM_BARS = 3 * STAGES + 8;
     static constexpr int RS_OFF = BAR_OFF + NUM_BARS * 8;
     static constexpr int TMEMPTR_OFF = RS_OFF + 2 * BM * 4;
     static constexpr int SMEM_BYTES = TMEMPTR_OFF + 16 + 1024;  // + alignment slack
@@ -65,7 +67,25 @@ struct TcParams {
     const int32_t* bias_add;  // raw writer only
     void* c;
     int ldc;
+    unsigned long long* trace;  // debug: 8 globaltimer stamps per CTA (Q8G_TC_TRACE), else null
 };
+
+__device__ __forceinline__ void trace_stamp(const TcParams& p, int slot) {
+    if (p.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[blockIdx.x * 8 + slot] = t;
+    }
+}
+// per-k-block stamps of CTA 0's first tile: [8192 + kb] producer issue,
+// [8192 + 64 + kb] MMA saw the stage land, [8192 + 128 + kb] MMA issued
+__device__ __forceinline__ void trace_kb(const TcParams& p, int which, int kb) {
+    if (p.trace && blockIdx.x == 0 && kb < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8192 + which * 64 + kb] = t;
+    }
+}
 
 constexpr int EPI_COLS = 16;  // columns per tcgen05.ld in the epilogue
 
@@ -142,6 +162,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) trace_stamp(p, 0);
     const uint32_t rank = CN > 1 ? ptx::cluster_ctarank() : 0;
     const uint32_t sA = base + Cfg::A_OFF, sB = base + Cfg::B_OFF;
     const uint32_t bar0 = base + Cfg::BAR_OFF;
@@ -151,6 +172,9 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
     auto rfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 4 + a); };
     auto rempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 6 + a); };
+    // row-sum warps have finished reading stage s (local; the MMA thread
+    // waits on it before its commit releases the stage cluster-wide)
+    auto rsdone_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + 8 + s); };
     int32_t* rs_buf = reinterpret_cast<int32_t*>(smem + Cfg::RS_OFF);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + Cfg::TMEMPTR_OFF);
 
@@ -158,7 +182,8 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         ptx::prefetch_tmap(&tmap_a);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full_bar(s), 1);
-            ptx::mbar_init(empty_bar(s), CN * (1 + (RS ? 4 : 0)));
+            ptx::mbar_init(empty_bar(s), CN);  // one MMA commit per cluster CTA
+            ptx::mbar_init(rsdone_bar(s), 4);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(tfull_bar(a), 1);
@@ -174,6 +199,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     if (CN > 1) ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
+    if (threadIdx.x == 0) trace_stamp(p, 1);
 
     const int num_clusters = gridDim.x / CN;
     const int cluster_id = blockIdx.x / CN;
@@ -204,6 +230,8 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                     const int8_t* src = p.pb + ((size_t)kb * p.np + n0) * kKBlock;
                     ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE_BYTES, src, Cfg::B_STAGE_BYTES,
                                         full_bar(stage), pol_b);
+                    if (kb == 0 && t == cluster_id) trace_stamp(p, 2);
+                    if (t == cluster_id) trace_kb(p, 0, kb);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -226,11 +254,15 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 for (int kb = 0; kb < p.nkb; ++kb) {
                     ptx::mbar_wait(full_bar(stage), phase);
                     ptx::tc_fence_after();
+                    if (kb == 0 && t == cluster_id) trace_stamp(p, 3);
+                    if (t == cluster_id) trace_kb(p, 1, kb);
                     const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE_BYTES);
                     const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE_BYTES);
 #pragma unroll
                     for (int ks = 0; ks < kKBlock / 32; ++ks)
                         ptx::mma_i8(d, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb | ks) != 0);
+                    if (t == cluster_id) trace_kb(p, 2, kb);
+                    if (RS) ptx::mbar_wait(rsdone_bar(stage), phase);  // row sums read this stage too
                     if (CN == 1)
                         ptx::tc_commit(empty_bar(stage));
                     else
@@ -241,6 +273,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                     }
                 }
                 ptx::tc_commit(tfull_bar(acc));
+                trace_stamp(p, 4);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -259,6 +292,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             const int n0 = (ng * CN + (int)rank) * BN;
             ptx::mbar_wait(tfull_bar(acc), acc_phase);
             ptx::tc_fence_after();
+            if (warp == 4 && lane == 0 && t == cluster_id) trace_stamp(p, 5);
             int32_t rowsum = 0;
             if (RS) {
                 ptx::mbar_wait(rfull_bar(acc), acc_phase);
@@ -281,6 +315,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+            if (warp == 4 && lane == 0) trace_stamp(p, 6);
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -310,14 +345,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                     sum = ptx::dp4a_uu(w.w, 0x01010101u, sum);
                 }
                 __syncwarp();
-                if (lane == 0) {
-                    if (CN == 1) {
-                        ptx::mbar_arrive(empty_bar(stage));
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < CN; ++q) ptx::mbar_arrive_cluster(empty_bar(stage), q);
-                    }
-                }
+                if (lane == 0) ptx::mbar_arrive(rsdone_bar(stage));
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -333,9 +361,13 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         }
     }
 
+    // reconverge every warp (lane 0 of the producer / MMA warps ran the role
+    // loop alone) before the CTA-wide aligned barrier
+    __syncwarp();
     ptx::tc_fence_before();
     __syncthreads();
     if (CN > 1) ptx::cluster_sync();
+    if (threadIdx.x == 0) trace_stamp(p, 7);
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
@@ -343,6 +375,21 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
 }
 
 // ------------------------------------------------------------------ host side
+
+// debug phase trace (env Q8G_TC_TRACE=1): 8 globaltimer stamps per CTA of the
+// most recent launch, read back with q8g_debug_tc_trace()
+constexpr int kTraceCtas = 1024;
+constexpr int kTraceWords = 8 * kTraceCtas + 256;  // + per-k-block stamps of CTA 0
+unsigned long long* tc_trace_buffer() {
+    static unsigned long long* buf = nullptr;
+    static bool enabled = getenv("Q8G_TC_TRACE") != nullptr;
+    if (!enabled) return nullptr;
+    if (!buf) {
+        if (cudaMalloc(&buf, sizeof(unsigned long long) * kTraceWords) != cudaSuccess) return nullptr;
+        cudaMemset(buf, 0, sizeof(unsigned long long) * kTraceWords);
+    }
+    return buf;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -431,6 +478,7 @@ cudaError_t launch_variant(const GemmArgs& g, cudaStream_t s) {
     p.bias_add = g.bias_add;
     p.c = g.c;
     p.ldc = g.ldc;
+    p.trace = tc_trace_buffer();
     const int total = p.num_m_tiles * p.num_n_groups;
     const int max_clusters = sm_count(dev) / CN;
     const int clusters = total < max_clusters ? total : max_clusters;
@@ -445,9 +493,9 @@ cudaError_t launch_variant(const GemmArgs& g, cudaStream_t s) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CN > 1 ? 1 : 0;  // plain launch unless A is multicast
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, p);
-    count_launch();
+    count_launch((CN > 1 || BN < 256) ? kFamGemmTcSmallM : kFamGemmTcLargeM);
     return e;
 }
 
@@ -462,13 +510,49 @@ cudaError_t launch_modes(const GemmArgs& g, cudaStream_t s) {
 
 }  // namespace
 
+int tc_trace_copy(unsigned long long* out, int max_ctas) {
+    unsigned long long* buf = tc_trace_buffer();
+    if (!buf) return 0;
+    // max_ctas > kTraceCtas: also copy the per-k-block stamps (kTraceWords total)
+    const int n = max_ctas < kTraceCtas ? max_ctas : kTraceCtas;
+    const size_t words = max_ctas > kTraceCtas ? (size_t)kTraceWords : (size_t)8 * n;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+    if (cudaMemcpy(out, buf, sizeof(unsigned long long) * words, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+    return n;
+}
+
 bool tc_supported(const GemmArgs& g) {
     return get_encode() != nullptr && (reinterpret_cast<uintptr_t>(g.a) % 16 == 0) && (g.lda % 16 == 0) &&
            g.k % 16 == 0 && g.k >= 16;
 }
 
+// Q8G_TC_CFG (tuning knob): force one tile config "BNxCN" for every
+// tensor-core launch: 32x8, 32x1, 64x4, 128x2, 256x1
+static int tc_cfg_override() {
+    static int v = [] {
+        const char* e = getenv("Q8G_TC_CFG");
+        if (!e) return 0;
+        std::string s(e);
+        if (s == "32x8") return 1;
+        if (s == "32x1") return 2;
+        if (s == "64x4") return 3;
+        if (s == "128x2") return 4;
+        if (s == "256x1") return 5;
+        return 0;
+    }();
+    return v;
+}
+
 cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
-    if (tile_kind == kSmallM) return launch_modes<32, 8, 10>(g, s);
+    switch (tc_cfg_override()) {
+        case 1: return launch_modes<32, 8, 10>(g, s);
+        case 2: return launch_modes<32, 1, 10>(g, s);
+        case 3: return launch_modes<64, 4, 8>(g, s);
+        case 4: return launch_modes<128, 2, 6>(g, s);
+        case 5: return launch_modes<256, 1, 4>(g, s);
+        default: break;
+    }
+    if (tile_kind == kSmallM) return launch_modes<32, 1, 10>(g, s);
     return launch_modes<256, 1, 4>(g, s);
 }
 

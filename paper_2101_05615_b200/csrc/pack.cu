@@ -86,7 +86,7 @@ cudaError_t launch_pack_b(const int8_t* b, int k, int n, int ldb, int8_t* packed
     if (e != cudaSuccess) return e;
     dim3 grid(np / kPackN, kp / kKBlock);
     pack_b_kernel<<<grid, 256, 0, s>>>(b, k, n, ldb, packed, np, colsum, max_abs);
-    count_launch();
+    count_launch(kFamPack);
     return cudaGetLastError();
 }
 
@@ -98,7 +98,7 @@ cudaError_t launch_unpack_b(const int8_t* packed, int k, int n, int kp, int np, 
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
     unpack_b_kernel<<<blocks, 256, 0, s>>>(packed, k, n, np, out, ldb);
-    count_launch();
+    count_launch(kFamPack);
     return cudaGetLastError();
 }
 

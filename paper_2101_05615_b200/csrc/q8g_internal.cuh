@@ -36,7 +36,20 @@ inline int ceil_div_i(int v, int d) { return (v + d - 1) / d; }
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
-void count_launch(int n = 1);
+// per-kernel-family launch counters (q8g_launch_stats): evidence of which
+// kernel actually ran
+enum KernelFamily : int {
+    kFamPack = 0,
+    kFamGemmSimt = 1,
+    kFamGemmTcSmallM = 2,
+    kFamGemmTcLargeM = 3,
+    kFamConvSimt = 4,
+    kFamConvTc = 5,
+    kFamDw = 6,
+    kFamDwTc = 7,
+    kFamCount = 8
+};
+void count_launch(int family);
 
 #define Q8G_CUDA_TRY(expr)                                   \
     do {                                                     \
@@ -150,6 +163,7 @@ struct GemmArgs {
 cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s);
 bool tc_supported(const GemmArgs& g);
+int tc_trace_copy(unsigned long long* out, int max_ctas);
 
 struct ConvArgs {
     const uint8_t* x;  // first image of the shard

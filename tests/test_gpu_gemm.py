@@ -112,7 +112,11 @@ def test_tensor_core_paths_raw(cuda, orc, m, n, k):
     pw = q8.prepack_weights(b)
     kc = q8.KernelCache()
     assert kc.tile(m, n, k, k) == (1 if m <= 128 else 2)
+    fam = "gemm_tc_small_m" if m <= 128 else "gemm_tc_large_m"
+    before = q8.launch_stats()
     assert (run_raw(a, pw, cache=kc) == orc.naive_gemm_i32(a, b)).all()
+    after = q8.launch_stats()
+    assert after[fam] == before[fam] + 1 and after["gemm_simt"] == before["gemm_simt"]
 
 
 def test_specialised_equals_generic(cuda, orc):

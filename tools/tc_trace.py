@@ -1,0 +1,68 @@
+"""Phase timeline of one tensor-core GEMM launch (debug; needs Q8G_TC_TRACE=1).
+
+Stamps (globaltimer ns) per CTA: 0 entry, 1 prologue done, 2 first TMA
+issued, 3 first stage landed (MMA), 4 last MMA commit, 5 epilogue start,
+6 epilogue done, 7 exit.  Prints min/median/max of each relative to the
+earliest entry over all CTAs.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+os.environ.setdefault("Q8G_TC_TRACE", "1")
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2101_05615_b200 as q8  # noqa: E402
+from paper_2101_05615_b200 import _lib  # noqa: E402
+
+NAMES = ["entry", "prologue", "tma0", "stage0", "mma_done", "epi_start", "epi_done", "exit"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=128)
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--k", type=int, default=4096)
+    args = ap.parse_args()
+    m, n, k = args.m, args.n, args.k
+    b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device="cuda")
+    a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device="cuda")
+    c = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    pw = q8.prepack_weights(b)
+    pipe = q8.OutputPipeline([q8.WriteRawI32()])
+    for _ in range(3):
+        q8.execute_gemm(a, pw, c, pipe)
+    torch.cuda.synchronize()
+    # flush L2 between the warm-up and the traced launch
+    junk = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    junk.fill_(1)
+    torch.cuda.synchronize()
+    q8.execute_gemm(a, pw, c, pipe)
+    torch.cuda.synchronize()
+    buf = (C.c_uint64 * (8 * 1024 + 256))()
+    nct = _lib.load().q8g_debug_tc_trace(buf, 2048)
+    allw = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+    t = allw[:8 * 1024].reshape(1024, 8)[:nct]
+    kbs = allw[8192:8192 + 192].reshape(3, 64)
+    used = t[:, 0] > 0
+    t = t[used]
+    t0 = t[:, 0].min()
+    print(f"cfg={os.environ.get('Q8G_TC_CFG', 'auto')} {m}x{n}x{k}: {len(t)} CTAs traced")
+    for i, nm in enumerate(NAMES):
+        col = t[:, i]
+        col = col[col > 0] - t0
+        if len(col):
+            print(f"  {nm:10s} min {col.min()/1e3:8.2f} us  med {np.median(col)/1e3:8.2f}  max {col.max()/1e3:8.2f}")
+    c0 = t[0, 0]
+    nk = int((kbs[0] > 0).sum())
+    print("  CTA0 per k-block (us from its entry): issue / landed / mma-issued")
+    for kb in range(nk):
+        print(f"    kb {kb:2d}: {(kbs[0, kb]-c0)/1e3:7.2f} {(kbs[1, kb]-c0)/1e3:7.2f} {(kbs[2, kb]-c0)/1e3:7.2f}")
+
+
+if __name__ == "__main__":
+    main()
