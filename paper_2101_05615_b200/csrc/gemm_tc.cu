@@ -510,6 +510,12 @@ cudaError_t launch_modes(const GemmArgs& g, cudaStream_t s) {
 
 }  // namespace
 
+bool make_tmap_a_cached(CUtensorMap* out, const uint8_t* a, int rows, int k, int lda, int box_rows) {
+    return cached_tmap_a(out, a, rows, k, lda, box_rows);
+}
+
+unsigned long long* tc_trace_buffer_ptr() { return tc_trace_buffer(); }
+
 int tc_trace_copy(unsigned long long* out, int max_ctas) {
     unsigned long long* buf = tc_trace_buffer();
     if (!buf) return 0;
@@ -538,6 +544,7 @@ static int tc_cfg_override() {
         if (s == "64x4") return 3;
         if (s == "128x2") return 4;
         if (s == "256x1") return 5;
+        if (s == "sk") return 6;
         return 0;
     }();
     return v;
@@ -550,9 +557,15 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
         case 3: return launch_modes<64, 4, 8>(g, s);
         case 4: return launch_modes<128, 2, 6>(g, s);
         case 5: return launch_modes<256, 1, 4>(g, s);
+        case 6:
+            if (splitk_supported(g)) return launch_gemm_splitk(g, s);
+            break;
         default: break;
     }
-    if (tile_kind == kSmallM) return launch_modes<32, 1, 10>(g, s);
+    if (tile_kind == kSmallM) {
+        if (splitk_supported(g)) return launch_gemm_splitk(g, s);
+        return launch_modes<32, 1, 10>(g, s);
+    }
     return launch_modes<256, 1, 4>(g, s);
 }
 
