@@ -618,6 +618,55 @@ int q8g_dw_filter_create(const int8_t* w_host, int c, const q8g_requant_params* 
         q8g_dw_filter_free(f);
         return cuda_fail(e, "dw_filter upload");
     }
+    // ---- tensor-core path constants (dwconv_tc.cu).  Exactness conditions:
+    // the float magic-number conversions need |adj| < 2^22, and the clamp
+    // folding needs 0 <= zp_c <= 255; otherwise the CUDA-core kernel runs.
+    {
+        std::vector<int32_t> zpw(c), cterm(c), corr(16 * c, 0);
+        std::vector<float> mult(c);
+        bool ok = p->zp_c >= 0 && p->zp_c <= 255;
+        int64_t max_bias = 0;
+        for (int ch = 0; ch < c; ++ch) {
+            const int64_t zw = p->zp_b_per_channel_host ? p->zp_b_per_channel_host[ch] : p->zp_b;
+            const int64_t b = p->bias_host ? p->bias_host[ch] : 0;
+            zpw[ch] = (int32_t)zw;
+            if (zw < -127 || zw > 127) ok = false;  // -zp_w must fit the s8 Z matrix
+            max_bias = std::max<int64_t>(max_bias, b < 0 ? -b : b);
+            const int64_t ct = b - (int64_t)p->zp_a * wsum[ch] + 9LL * p->zp_a * zw;
+            cterm[ch] = (int32_t)(ct + 0x4B400000LL);
+            mult[ch] = rec[ch].mf;
+            for (int cls = 1; cls < 16; ++cls) {
+                int64_t s = 0;
+                for (int t = 0; t < 9; ++t) {
+                    const int kh = t / 3, kw = t % 3;
+                    const bool padded = ((cls & 1) && kh == 0) || ((cls & 2) && kh == 2) || ((cls & 4) && kw == 0) ||
+                                        ((cls & 8) && kw == 2);
+                    if (padded) s += (int64_t)w_host[t * c + ch] - zw;
+                }
+                corr[cls * c + ch] = (int32_t)(p->zp_a * s);
+            }
+        }
+        // |adj| <= 9 * 255 * (128 + |zp_w|) + |bias| must stay below 2^22
+        if (9LL * 255 * 256 + max_bias >= (1LL << 22)) ok = false;
+        f->lo = p->relu ? 0.0f : (float)(-p->zp_c);
+        f->hi = (float)(255 - p->zp_c);
+        if (ok) {
+            if ((e = cudaMalloc(&f->zpw_dev, sizeof(int32_t) * c)) != cudaSuccess ||
+                (e = cudaMalloc(&f->cterm_dev, sizeof(int32_t) * c)) != cudaSuccess ||
+                (e = cudaMalloc(&f->mult_dev, sizeof(float) * c)) != cudaSuccess ||
+                (e = cudaMalloc(&f->corr_dev, sizeof(int32_t) * 16 * c)) != cudaSuccess ||
+                (e = cudaMemcpy(f->zpw_dev, zpw.data(), sizeof(int32_t) * c, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(f->cterm_dev, cterm.data(), sizeof(int32_t) * c, cudaMemcpyHostToDevice)) !=
+                    cudaSuccess ||
+                (e = cudaMemcpy(f->mult_dev, mult.data(), sizeof(float) * c, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(f->corr_dev, corr.data(), sizeof(int32_t) * 16 * c, cudaMemcpyHostToDevice)) !=
+                    cudaSuccess) {
+                q8g_dw_filter_free(f);
+                return cuda_fail(e, "dw_filter tensor-core tables");
+            }
+            f->tc_ok = true;
+        }
+    }
     *out = f;
     return Q8G_OK;
 }
@@ -627,6 +676,10 @@ int q8g_dw_filter_free(q8g_dw_filter* f) {
     DeviceGuard dg(f->device);
     if (f->w) cudaFree(f->w);
     if (f->rec) cudaFree(f->rec);
+    if (f->zpw_dev) cudaFree(f->zpw_dev);
+    if (f->cterm_dev) cudaFree(f->cterm_dev);
+    if (f->mult_dev) cudaFree(f->mult_dev);
+    if (f->corr_dev) cudaFree(f->corr_dev);
     delete f;
     return Q8G_OK;
 }

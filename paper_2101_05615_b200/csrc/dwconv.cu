@@ -83,6 +83,8 @@ __global__ void dw_scalar_kernel(const uint8_t* __restrict__ x, int nb, int h, i
 
 cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c, const q8g_dw_filter* f,
                              uint8_t* y, cudaStream_t s) {
+    if (f->tc_ok && dw_tc_supported(h, w, c, f->zp_a) && getenv("Q8G_DW_SIMT") == nullptr)
+        return launch_dwconv3x3_tc(x, nb, h, w, c, f, y, s);
     int dev = 0;
     cudaGetDevice(&dev);
     const int blocks = sm_count(dev) * 8;

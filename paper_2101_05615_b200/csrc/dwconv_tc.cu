@@ -1,0 +1,418 @@
+// dwconv_tc.cu — depthwise 3x3 / stride 1 / pad 1 NHWC on the tensor cores
+// (BASELINE config C4, the HBM-bound path).
+//
+// Semantics: SURVEY.md App. A D3 (no reference symbol).  For output (n,h,w,c):
+//   adj = sum_t x_t*(w[t,c] - zp_w[c]) + bias[c] - zp_a*wsum[c] + 9*zp_a*zp_w[c]
+// with padded taps reading x = zp_a, then the F32_RNE requant.
+//
+// Design (why it is not a CUDA-core kernel): at 70% of HBM the whole 32x112x
+// 112x256 layer has ~45 us, i.e. ~11-16 issue slots per output for 9 MACs,
+// the sum_x term and the requant.  Here the MACs and the -zp_w*sum_x term run
+// on tcgen05: for a group of 16 channels the depthwise sum is a GEMM with a
+// block-diagonal B (K = 9 taps x 16 channels, N = 16), and
+//   D = A x W_g + A x Z_g,  Z_g[(t,c), c'] = -zp_w[c'] * delta(c, c')
+// accumulates both in the same TMEM tile.  The A operand is never
+// materialised: the CTA loads a halo of R+2 input rows (padded width W+2,
+// 16 channels per pixel, out-of-range taps zero-filled by TMA) and each MMA
+// K-step (two taps) reads two shifted windows of that halo through a
+// no-swizzle K-major descriptor whose leading-byte offset is the distance
+// between the taps.  The zero-filled padding is corrected exactly per border
+// class (corr[class][c] = zp_a * sum_{padded t} (w[t,c] - zp_w[c])).  CUDA
+// cores only run the requantization (magic-number float conversions, ~8
+// issue slots per output) and the 16-byte stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "ptx.cuh"
+#include "q8g_internal.cuh"
+
+namespace q8g {
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder();
+unsigned long long* tc_trace_buffer_ptr();
+
+namespace {
+
+constexpr int G = 16;          // channels per group (MMA N)
+constexpr int TAPS = 10;       // 9 taps + one zero-weight tap (K = 160 = 5 x 32)
+constexpr int ROWS = 8;        // output rows per work unit
+constexpr int NBUF = 3;        // halo buffers in flight
+constexpr int MAXW = 254;      // padded width <= 256 (TMA box limit)
+constexpr int EPI_WARPS = 8;
+
+struct DwParams {
+    int nb, h, w, c;           // NHWC dims
+    int wp;                    // padded width w + 2
+    int groups;                // c / 16
+    int rblocks;               // ceil(h / ROWS)
+    int tiles;                 // M tiles of 128 positions per unit
+    int units;                 // nb * rblocks * groups
+    int halo_bytes;            // (ROWS + 2) * wp * 16
+    const int8_t* wt;          // [9][c]
+    const int32_t* zpw;        // [c]
+    const int32_t* cterm;      // [c]: bias - zp_a*wsum + 9*zp_a*zp_w + float magic bits
+    const float* mult;         // [c]
+    const int32_t* corr;       // [16][c] border-class corrections
+    float lo, hi;              // clamp bounds in the pre-zp_c domain
+    int32_t zp_c;
+    uint8_t* y;
+    unsigned long long* trace;  // debug (Q8G_TC_TRACE): per-unit stamps of CTA 0, else null
+};
+
+// CTA 0, unit i < 64: [8192 + 64*which + i]; which: 0 halo TMA issued, 1 halo
+// landed (MMA), 2 MMAs issued, 3 epilogue got the accumulators, 4 epilogue done
+__device__ __forceinline__ void dw_stamp(const DwParams& p, int which, int i) {
+    if (p.trace && blockIdx.x == 0 && i < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8192 + which * 64 + i] = t;
+    }
+}
+
+__host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
+
+// smem layout
+struct DwLayout {
+    int halo_off, halo_stride, b_off, corr_off, bar_off, tmemptr_off, total;
+};
+__host__ __device__ inline DwLayout dw_layout(int halo_bytes, int groups) {
+    DwLayout L;
+    L.halo_off = 1024;  // 1 KB front guard: tap windows may start up to one pixel early
+    L.halo_stride = align_up(halo_bytes + 2048, 1024);  // + tail guard for the last tile's rows
+    L.b_off = L.halo_off + NBUF * L.halo_stride;
+    // per group: B = [W rows 0-15 | Z rows 16-31], TAPS x 32 rows x 16 B
+    L.corr_off = L.b_off + groups * TAPS * 2 * G * 16;
+    L.bar_off = L.corr_off + 16 * groups * G * 4;  // [16 classes][c] int32
+    L.tmemptr_off = L.bar_off + (2 * NBUF + 4) * 8;
+    L.total = L.tmemptr_off + 16 + 1024;
+    return L;
+}
+
+// no-swizzle K-major UMMA descriptor: core matrices of 8 rows x 16 B (rows
+// contiguous), SBO between 8-row groups, LBO between the two 16-byte K halves
+__device__ __forceinline__ uint64_t kmajor_noswz_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);  // layout type 0 = SWIZZLE_NONE
+}
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    // low bytes of a,b,c,d -> one word
+    const uint32_t ab = __byte_perm(a, b, 0x0040);
+    const uint32_t cd = __byte_perm(c, d, 0x0040);
+    return __byte_perm(ab, cd, 0x5410);
+}
+
+__global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
+    dwconv_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const DwParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    const uint32_t base = (raw_addr + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base - raw_addr);
+    const DwLayout L = dw_layout(p.halo_bytes, p.groups);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t bar0 = base + L.bar_off;
+    auto full_bar = [&](int b) { return bar0 + 8u * b; };
+    auto empty_bar = [&](int b) { return bar0 + 8u * (NBUF + b); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + 2 + a); };
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmemptr_off);
+
+    // ---- block-diagonal B = [W | Z] for every channel group (built once):
+    // rows 0-15 W[t][c'] on the diagonal, rows 16-31 -zp_w[c'] on the diagonal
+    for (int idx = threadIdx.x; idx < p.groups * TAPS * 2 * G; idx += blockDim.x) {
+        const int g = idx / (TAPS * 2 * G), rem = idx % (TAPS * 2 * G);
+        const int t = rem / (2 * G), row = rem % (2 * G);
+        const int oc = row % G;  // output channel within the group
+        const int ch = g * G + oc;
+        uint32_t v[4] = {0, 0, 0, 0};
+        if (t < 9) {
+            const uint32_t byte = row < G ? (uint32_t)(uint8_t)p.wt[t * p.c + ch]
+                                          : (uint32_t)(uint8_t)(int8_t)(-p.zpw[ch]);
+            v[oc / 4] = byte << (8 * (oc % 4));
+        }
+        // [g][tap][row][16 B]
+        *reinterpret_cast<uint4*>(smem + L.b_off + ((g * TAPS + t) * 2 * G + row) * 16) =
+            make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    // per border class: cterm (bias, offsets, float magic) + padding correction
+    for (int i = threadIdx.x; i < 16 * p.c; i += blockDim.x)
+        reinterpret_cast<int32_t*>(smem + L.corr_off)[i] = p.corr[i] + p.cterm[i % p.c];
+    // the halo guards must hold finite data (they only feed garbage rows)
+    for (int i = threadIdx.x; i < L.b_off / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_x);
+        for (int b = 0; b < NBUF; ++b) {
+            ptx::mbar_init(full_bar(b), 1);
+            ptx::mbar_init(empty_bar(b), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull_bar(a), 1);
+            ptx::mbar_init(tempty_bar(a), EPI_WARPS);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_ptr;
+    const int per_img = p.rblocks * p.groups;
+
+    if (warp == 0) {
+        // ------------------------------------------------ halo producer
+        // (whole warp runs the loop; one elected lane issues)
+        {
+            int b = 0;
+            uint32_t ph = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const int n = u / per_img, rem = u % per_img;
+                const int rb = rem / p.groups, g = rem % p.groups;
+                ptx::mbar_wait(empty_bar(b), ph ^ 1);
+                if (ptx::elect_one()) {
+                    ptx::mbar_arrive_expect_tx(full_bar(b), (uint32_t)p.halo_bytes);
+                    // box {16 ch, wp px, ROWS+2 rows, 1}: starts at (row r0-1, col -1)
+                    tma_load_4d(base + L.halo_off + b * L.halo_stride, &tmap_x, g * G, -1, rb * ROWS - 1, n,
+                                full_bar(b));
+                    dw_stamp(p, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
+                }
+                __syncwarp();
+                if (++b == NBUF) {
+                    b = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        // (whole warp runs the loop with warp-uniform descriptors; one elected
+        // lane issues the tcgen05 instructions)
+        {
+            constexpr uint32_t idesc = ptx::idesc_u8s8_s32<128, 2 * G>();  // N = 32: [W | Z]
+            // descriptor templates: A for K-step s (taps 2s, 2s+1) relative to
+            // halo position 0 -- tap t reads halo position q + (t/3)*wp + t%3 - 1,
+            // tap 9 has zero weights and reuses the next pixel; B per K-step
+            uint64_t a_t[TAPS / 2], b_t[TAPS / 2];
+#pragma unroll
+            for (int s = 0; s < TAPS / 2; ++s) {
+                const int t0 = 2 * s, t1 = 2 * s + 1;
+                const int sh0 = (t0 / 3) * p.wp + (t0 % 3) - 1;
+                const int sh1 = t1 < 9 ? (t1 / 3) * p.wp + (t1 % 3) - 1 : sh0 + 1;
+                // +1: keep the template's start field non-negative (sh0 >= -1);
+                // the per-tile base below is one position earlier to compensate
+                a_t[s] = kmajor_noswz_desc((uint32_t)((sh0 + 1) * 16), (uint32_t)((sh1 - sh0) * 16), 128);
+                // B: per tap 32 rows x 16 B = 512 B; K-step s = taps 2s, 2s+1
+                b_t[s] = kmajor_noswz_desc((uint32_t)(s * 2 * (2 * G) * 16), 2 * G * 16, 128);
+            }
+            int b = 0, acc = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const int g = (u % per_img) % p.groups;
+                ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
+                ptx::mbar_wait(full_bar(b), ph);
+                ptx::tc_fence_after();
+                const int ui = (u - (int)blockIdx.x) / (int)gridDim.x;
+                if (lane == 0) dw_stamp(p, 1, ui);
+                // start-address fields are in 16-byte units (low 14 bits)
+                const uint64_t halo16 = (base + L.halo_off + b * L.halo_stride) >> 4;
+                const uint64_t b16 = (base + L.b_off + g * TAPS * 2 * G * 16) >> 4;
+                for (int tile = 0; tile < p.tiles; ++tile) {
+                    // accumulator: 32 columns per tile (16 acc + 16 -zp_w*sum_x)
+                    const uint32_t d = tmem_base + (uint32_t)(acc * 256 + tile * 2 * G);
+                    const uint64_t a16 = halo16 - 1 + (uint64_t)(tile * 128);  // 128 positions x 16 B
+                    if (ptx::elect_one()) {
+#pragma unroll
+                        for (int s = 0; s < TAPS / 2; ++s)
+                            ptx::mma_i8(d, a_t[s] + a16, b_t[s] + b16, idesc, s != 0);
+                    }
+                    __syncwarp();
+                }
+                if (ptx::elect_one()) {
+                    ptx::tc_commit(empty_bar(b));
+                    ptx::tc_commit(tfull_bar(acc));
+                    dw_stamp(p, 2, ui);
+                }
+                __syncwarp();
+                if (++b == NBUF) {
+                    b = 0;
+                    ph ^= 1;
+                }
+                if (++acc == 2) {
+                    acc = 0;
+                    aph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // (TMEM allocator; idle during the main loop)
+    } else if (warp >= 4) {
+        // ------------------------------------------------ requant epilogue
+        const int ew = warp - 4;          // 0..7
+        const int quarter = ew % 4;       // TMEM lanes [32*quarter, +32)
+        const int half = ew / 4;          // even / odd tiles
+        const int r = quarter * 32 + lane;
+        const float magic = 12582912.0f;  // 1.5 * 2^23
+        // this thread's output position in each of its tiles (unit-independent)
+        int t_orow[4], t_ocol[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int q = (half + 2 * i) * 128 + r;
+            t_orow[i] = q / p.wp;
+            t_ocol[i] = q % p.wp - 1;
+        }
+        // with a zero clamp floor (ReLU) every packed byte r satisfies
+        // r + zp_c <= 255, so zp_c is added once per packed word (no carries)
+        const bool relu_fast = p.lo == 0.0f;
+        const uint32_t zp4 = relu_fast ? (uint32_t)p.zp_c * 0x01010101u : 0u;
+        const uint32_t zp1 = relu_fast ? 0u : (uint32_t)p.zp_c;
+        const int32_t* corr_s = reinterpret_cast<const int32_t*>(smem + L.corr_off);
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const int n = u / per_img, rem = u % per_img;
+            const int rb = rem / p.groups, g = rem % p.groups;
+            const int c0 = g * G;
+            float mf[G];
+#pragma unroll
+            for (int j = 0; j < G; ++j) mf[j] = __ldg(p.mult + c0 + j);
+            ptx::mbar_wait(tfull_bar(acc), aph);
+            ptx::tc_fence_after();
+            const int ui = (u - (int)blockIdx.x) / (int)gridDim.x;
+            if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
+            // requantize one tile's 16 channels for this thread's position
+            auto emit = [&](const uint32_t (&v)[2 * G], int i) {
+                const int orow = t_orow[i], ocol = t_ocol[i];
+                const int oh = rb * ROWS + orow;
+                if (orow >= ROWS || oh >= p.h || ocol < 0 || ocol >= p.w) return;
+                const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) |
+                                (ocol == p.w - 1 ? 8 : 0);
+                // class row = cterm (+ zero-padding correction), float magic bits folded in
+                const int4* crow = reinterpret_cast<const int4*>(corr_s + cls * p.c + c0);
+                uint32_t qv[G];
+#pragma unroll
+                for (int j4 = 0; j4 < G / 4; ++j4) {
+                    const int4 cc = crow[j4];
+                    const int32_t cj[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = j4 * 4 + k;
+                        const int32_t bits = (int32_t)(v[j] + v[G + j]) + cj[k];
+                        float x = __fmul_rn(__fsub_rn(__int_as_float(bits), magic), mf[j]);
+                        x = fminf(fmaxf(x, p.lo), p.hi);
+                        qv[j] = (uint32_t)__float_as_int(__fadd_rn(x, magic)) + zp1;
+                    }
+                }
+                uint4 out;
+                out.x = pack4(qv[0], qv[1], qv[2], qv[3]) + zp4;
+                out.y = pack4(qv[4], qv[5], qv[6], qv[7]) + zp4;
+                out.z = pack4(qv[8], qv[9], qv[10], qv[11]) + zp4;
+                out.w = pack4(qv[12], qv[13], qv[14], qv[15]) + zp4;
+                uint8_t* dst = p.y + ((((size_t)n * p.h + oh) * p.w + ocol) * p.c + c0);
+                *reinterpret_cast<uint4*>(dst) = out;
+            };
+            // two tiles' TMEM loads in flight per step (ILP)
+#pragma unroll
+            for (int i = 0; i < 4; i += 2) {
+                const int ta = half + 2 * i, tb = ta + 2;
+                if (ta >= p.tiles) break;  // warp-uniform
+                uint32_t va[2 * G], vb[2 * G];  // [0,16): sum x*w, [16,32): -zp_w * sum x
+                const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
+                ptx::tmem_ld_32x32b_x32(lane_base + (uint32_t)(ta * 2 * G), va);
+                if (tb < p.tiles) ptx::tmem_ld_32x32b_x32(lane_base + (uint32_t)(tb * 2 * G), vb);
+                ptx::tmem_ld_wait();
+                emit(va, i);
+                if (tb < p.tiles) emit(vb, i + 1);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+            if (ew == 0 && lane == 0) dw_stamp(p, 4, ui);
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    }
+
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem_base);
+    }
+}
+
+}  // namespace
+
+bool dw_tc_supported(int h, int w, int c, int32_t zp_a) {
+    (void)zp_a;
+    // one unit's tiles (ROWS rows of w+2 positions) must fit a 128-column TMEM buffer
+    return c % G == 0 && w + 2 <= MAXW && (ROWS * (w + 2) + 127) / 128 * G <= 128 && h >= 1 &&
+           tmap_encoder() != nullptr &&
+           dw_layout((ROWS + 2) * (w + 2) * G, c / G).total <= 232448;
+}
+
+cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, const q8g_dw_filter* f, uint8_t* y,
+                                cudaStream_t s) {
+    auto enc = tmap_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap tmap;
+    cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)nb};
+    cuuint64_t strides[3] = {(cuuint64_t)c, (cuuint64_t)w * c, (cuuint64_t)h * w * c};
+    cuuint32_t box[4] = {(cuuint32_t)G, (cuuint32_t)(w + 2), (cuuint32_t)(ROWS + 2), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    DwParams p;
+    p.nb = nb;
+    p.h = h;
+    p.w = w;
+    p.c = c;
+    p.wp = w + 2;
+    p.groups = c / G;
+    p.rblocks = (h + ROWS - 1) / ROWS;
+    p.tiles = (ROWS * p.wp + 127) / 128;
+    p.units = nb * p.rblocks * p.groups;
+    p.halo_bytes = (ROWS + 2) * p.wp * G;
+    p.wt = f->w;
+    p.zpw = f->zpw_dev;
+    p.cterm = f->cterm_dev;
+    p.mult = f->mult_dev;
+    p.corr = f->corr_dev;
+    p.lo = f->lo;
+    p.hi = f->hi;
+    p.zp_c = f->zp_c;
+    p.y = y;
+    p.trace = tc_trace_buffer_ptr();
+    const DwLayout L = dw_layout(p.halo_bytes, p.groups);
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(dwconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = true;
+    }
+    int grid = sm_count(dev);
+    if (grid > p.units) grid = p.units;
+    dwconv_tc_kernel<<<grid, 128 + 32 * EPI_WARPS, L.total, s>>>(tmap, p);
+    count_launch(kFamDwTc);
+    return cudaGetLastError();
+}
+
+}  // namespace q8g

@@ -169,47 +169,52 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     if (threadIdx.x == 0) sk_stamp(p, 1);
 
     if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t pol_b = ptx::policy_evict_first();  // weights streamed once
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int kb = kb0; kb < kb1; ++kb) {
-                ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+        // whole warp runs the loop; one elected lane issues (ptx::elect_one)
+        const uint64_t pol_b = ptx::policy_evict_first();  // weights streamed once
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+            if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(full_bar(stage), A_STAGE + Cfg::B_STAGE);
                 ptx::tma_load_2d(sA + stage * A_STAGE, &tmap_a, kb * kKBlock, m0, full_bar(stage));
                 ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE, p.pb + ((size_t)kb * p.np + n0) * kKBlock,
                                     Cfg::B_STAGE, full_bar(stage), pol_b);
                 if (kb == kb0) sk_stamp(p, 2);
                 sk_kb(p, 0, kb - kb0);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
             }
         }
-        __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_u8s8_s32<BM, BN>();
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int kb = kb0; kb < kb1; ++kb) {
-                ptx::mbar_wait(full_bar(stage), phase);
-                ptx::tc_fence_after();
+        constexpr uint32_t idesc = ptx::idesc_u8s8_s32<BM, BN>();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(full_bar(stage), phase);
+            ptx::tc_fence_after();
+            const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE);
+            const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE);
+            if (ptx::elect_one()) {
                 if (kb == kb0) sk_stamp(p, 3);
                 sk_kb(p, 1, kb - kb0);
-                const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE);
-                const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE);
 #pragma unroll
                 for (int ks = 0; ks < kKBlock / 32; ++ks)
                     ptx::mma_i8(tmem_base, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
-                if (RS) ptx::mbar_wait(rsdone_bar(stage), phase);
-                ptx::tc_commit(empty_bar(stage));
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
             }
+            __syncwarp();
+            if (RS) ptx::mbar_wait(rsdone_bar(stage), phase);
+            if (ptx::elect_one()) ptx::tc_commit(empty_bar(stage));  // same lane as the MMAs
+            __syncwarp();
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        if (ptx::elect_one()) {
             ptx::tc_commit(tfull);
             sk_stamp(p, 4);
         }

@@ -207,77 +207,88 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            const uint64_t pol_b = ptx::policy_evict_last();  // weights are re-read by every M tile
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = cluster_id; t < total; t += num_clusters) {
-                const int m_blk = t / p.num_n_groups, ng = t % p.num_n_groups;
-                const int m0 = m_blk * BM;
-                const int n0 = (ng * CN + (int)rank) * BN;
-                for (int kb = 0; kb < p.nkb; ++kb) {
-                    ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+        // (whole warp runs the loop with warp-uniform values; one elected lane
+        // issues -- see ptx::elect_one)
+        const uint64_t pol_b = ptx::policy_evict_last();  // weights are re-read by every M tile
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = cluster_id; t < total; t += num_clusters) {
+            const int m_blk = t / p.num_n_groups, ng = t % p.num_n_groups;
+            const int m0 = m_blk * BM;
+            const int n0 = (ng * CN + (int)rank) * BN;
+            for (int kb = 0; kb < p.nkb; ++kb) {
+                ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+                const uint32_t a_dst = sA + stage * A_STAGE_BYTES;
+                const int8_t* src = p.pb + ((size_t)kb * p.np + n0) * kKBlock;
+                if (ptx::elect_one()) {
                     ptx::mbar_arrive_expect_tx(full_bar(stage), A_STAGE_BYTES + Cfg::B_STAGE_BYTES);
-                    const uint32_t a_dst = sA + stage * A_STAGE_BYTES;
                     if (CN == 1) {
                         ptx::tma_load_2d(a_dst, &tmap_a, kb * kKBlock, m0, full_bar(stage));
                     } else {
                         constexpr int SLICE = BM / CN;
                         ptx::tma_load_2d_mc(a_dst + rank * SLICE * kKBlock, &tmap_a, kb * kKBlock,
-                                            m0 + (int)rank * SLICE, full_bar(stage),
-                                            (uint16_t)((1u << CN) - 1));
+                                            m0 + (int)rank * SLICE, full_bar(stage), (uint16_t)((1u << CN) - 1));
                     }
-                    const int8_t* src = p.pb + ((size_t)kb * p.np + n0) * kKBlock;
-                    ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE_BYTES, src, Cfg::B_STAGE_BYTES,
-                                        full_bar(stage), pol_b);
+                    ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE_BYTES, src, Cfg::B_STAGE_BYTES, full_bar(stage),
+                                        pol_b);
                     if (kb == 0 && t == cluster_id) trace_stamp(p, 2);
                     if (t == cluster_id) trace_kb(p, 0, kb);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_u8s8_s32<BM, BN>();
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int t = cluster_id; t < total; t += num_clusters) {
-                ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        constexpr uint32_t idesc = ptx::idesc_u8s8_s32<BM, BN>();
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cluster_id; t < total; t += num_clusters) {
+            ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+            for (int kb = 0; kb < p.nkb; ++kb) {
+                ptx::mbar_wait(full_bar(stage), phase);
                 ptx::tc_fence_after();
-                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
-                for (int kb = 0; kb < p.nkb; ++kb) {
-                    ptx::mbar_wait(full_bar(stage), phase);
-                    ptx::tc_fence_after();
+                const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE_BYTES);
+                const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE_BYTES);
+                if (ptx::elect_one()) {
                     if (kb == 0 && t == cluster_id) trace_stamp(p, 3);
                     if (t == cluster_id) trace_kb(p, 1, kb);
-                    const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE_BYTES);
-                    const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE_BYTES);
 #pragma unroll
                     for (int ks = 0; ks < kKBlock / 32; ++ks)
                         ptx::mma_i8(d, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb | ks) != 0);
                     if (t == cluster_id) trace_kb(p, 2, kb);
-                    if (RS) ptx::mbar_wait(rsdone_bar(stage), phase);  // row sums read this stage too
+                }
+                __syncwarp();
+                // the stage is released only after the row-sum warps read it too;
+                // the same (lowest) lane is elected again, so it commits its MMAs
+                if (RS) ptx::mbar_wait(rsdone_bar(stage), phase);
+                if (ptx::elect_one()) {
                     if (CN == 1)
                         ptx::tc_commit(empty_bar(stage));
                     else
                         ptx::tc_commit_mc(empty_bar(stage), (uint16_t)((1u << CN) - 1));
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (ptx::elect_one()) {
                 ptx::tc_commit(tfull_bar(acc));
                 trace_stamp(p, 4);
-                if (++acc == 2) {
-                    acc = 0;
-                    acc_phase ^= 1;
-                }
+            }
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
 // debug phase trace (env Q8G_TC_TRACE=1): 8 globaltimer stamps per CTA of the
 // most recent launch, read back with q8g_debug_tc_trace()
 constexpr int kTraceCtas = 1024;
-constexpr int kTraceWords = 8 * kTraceCtas + 256;  // + per-k-block stamps of CTA 0
+constexpr int kTraceWords = 8 * kTraceCtas + 512;  // + per-k-block / per-unit stamps of CTA 0
 unsigned long long* tc_trace_buffer() {
     static unsigned long long* buf = nullptr;
     static bool enabled = getenv("Q8G_TC_TRACE") != nullptr;
@@ -515,6 +526,8 @@ bool make_tmap_a_cached(CUtensorMap* out, const uint8_t* a, int rows, int k, int
 }
 
 unsigned long long* tc_trace_buffer_ptr() { return tc_trace_buffer(); }
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() { return get_encode(); }
 
 int tc_trace_copy(unsigned long long* out, int max_ctas) {
     unsigned long long* buf = tc_trace_buffer();

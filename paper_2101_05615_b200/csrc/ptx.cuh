@@ -21,6 +21,24 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     return r;
 }
 
+// one elected lane of a converged warp (elect.sync): lets a whole warp run a
+// role loop with warp-uniform values while a single lane issues tcgen05 / TMA
+// (a lane-0-only branch makes the compiler wrap each tcgen05.mma in an
+// ELECT + BRA.U.ANY uniformity loop with R2UR moves)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t"
+        ".reg .b32 %%rx;\n\t"
+        ".reg .pred %%px;\n\t"
+        "elect.sync %%rx|%%px, %1;\n\t"
+        "@%%px mov.s32 %0, 1;\n\t"
+        "}"
+        : "+r"(pred)
+        : "r"(0xFFFFFFFFu));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

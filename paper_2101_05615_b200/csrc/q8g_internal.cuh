@@ -112,6 +112,13 @@ struct q8g_dw_filter {
     int relu = 0;
     int8_t* w = nullptr;             // device [9][c]
     q8g::EpiRecord* rec = nullptr;   // device, c records (fp32 mult)
+    // tensor-core path (dwconv_tc.cu); tc_ok false -> CUDA-core kernel
+    bool tc_ok = false;
+    int32_t* zpw_dev = nullptr;      // [c]
+    int32_t* cterm_dev = nullptr;    // [c] bias - zp_a*wsum + 9*zp_a*zp_w + 0x4B400000
+    float* mult_dev = nullptr;       // [c]
+    int32_t* corr_dev = nullptr;     // [16][c] zero-padding corrections per border class
+    float lo = 0.f, hi = 255.f;      // clamp bounds before + zp_c
 };
 
 namespace q8g {
@@ -180,6 +187,9 @@ cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s);
 
 cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c,
                              const q8g_dw_filter* f, uint8_t* y, cudaStream_t s);
+bool dw_tc_supported(int h, int w, int c, int32_t zp_a);
+cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, const q8g_dw_filter* f,
+                                uint8_t* y, cudaStream_t s);
 
 int sm_count(int device);
 
