@@ -224,6 +224,9 @@ int q8g_packed_b_replicate(const q8g_packed_b* src, int device, q8g_packed_b** o
     pb->device = device;
     pb->data = nullptr;
     pb->colsum_dev = nullptr;
+    pb->conv_img = nullptr;  // rebuilt lazily on the replica's device
+    pb->conv_img_c = 0;
+    pb->conv_img_bytes = 0;
     pb->colsum_host = (int32_t*)malloc(sizeof(int32_t) * src->np);
     memcpy(pb->colsum_host, src->colsum_host, sizeof(int32_t) * src->np);
     cudaError_t e;
@@ -283,6 +286,7 @@ int q8g_free_packed_b(q8g_packed_b* pb) {
     DeviceGuard dg(pb->device);
     if (pb->data) cudaFree(pb->data);
     if (pb->colsum_dev) cudaFree(pb->colsum_dev);
+    if (pb->conv_img) cudaFree(pb->conv_img);
     free(pb->colsum_host);
     delete pb;
     return Q8G_OK;

@@ -124,6 +124,9 @@ cudaError_t launch_conv3x3_simt(const ConvArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s) { return launch_conv3x3_simt(a, s); }
+cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s) {
+    if (conv_tc_supported(a) && getenv("Q8G_CONV_SIMT") == nullptr) return launch_conv3x3_tc(a, s);
+    return launch_conv3x3_simt(a, s);
+}
 
 }  // namespace q8g

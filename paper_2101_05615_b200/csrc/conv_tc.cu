@@ -1,0 +1,525 @@
+// conv_tc.cu — 3x3 / stride 1 / pad 1 NHWC convolution as an implicit GEMM on
+// the tensor cores (BASELINE config C3), requantization fused.
+//
+// Semantics: SURVEY.md App. A D2 (no reference symbol; im2col is a reference
+// non-goal): GEMM rows = output pixels, k = (kh*3+kw)*C + c,
+// padded taps read zp_a and count in the row sums, weights = the packed
+// K = 9C x N = OC matrix, epilogue table from q8g_epilogue_create (K = 9C).
+//
+// Design: im2col is never materialised.  A work unit is (image, ROWS output
+// rows); TMA loads a halo of ROWS+2 input rows x (W+2) padded positions,
+// stored as C/16 planes of 16 channels (16 B per position), out-of-range
+// taps zero-filled.  For tap t and channel pair-of-planes j the MMA A
+// operand is the window starting at position q + (t/3)*(W+2) + t%3 - 1 of
+// planes 2j, 2j+1: a SWIZZLE_NONE K-major descriptor with LBO = the plane
+// distance.  B (built once per CTA in smem from the packed weights) has the
+// OC output channels plus one all-ones column, so the tensor core also
+// produces the row sum of the zero-filled A.  The exact correction for
+// zero- instead of zp_a-padding depends only on which taps of a pixel are
+// padded (16 border classes):
+//   corr[cls][j] = zp_a * sum_{t padded} (wsum_t[j] - C * zp_b[j])   (requant)
+//   corr[cls][j] = zp_a * sum_{t padded} wsum_t[j]                   (raw)
+// and adj = D[j] - zp_b[j] * D[ones] + c[j] + corr[cls][j].
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "ptx.cuh"
+#include "q8g_internal.cuh"
+#include "requant.cuh"
+
+namespace q8g {
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder();
+unsigned long long* tc_trace_buffer_ptr();
+
+namespace {
+
+constexpr int ROWS = 2;      // output rows per unit (ROWS * (W+2) <= 128 -> one M tile)
+constexpr int NBUF = 3;      // halo buffers in flight
+constexpr int EPI_WARPS = 8;  // two warpgroups, one per TMEM accumulator buffer
+
+struct CvParams {
+    int nb, h, w, c, oc;
+    int wp;            // w + 2
+    int planes;        // c / 16
+    int nq;            // MMA N = round_up(oc, 16) + 16 (ones column at index oc_pad)
+    int oc_pad;        // round_up(oc, 16)
+    int rblocks, units;
+    int plane_bytes;   // (ROWS+2) * wp * 16, padded to 128
+    int halo_bytes;    // planes * plane_bytes
+    const int8_t* pb;  // packed weights
+    int np;            // packed N pad
+    const uint8_t* img;  // operand image: smem B layout + [9][oc_pad] tap sums
+    int img_bytes;
+    const EpiRecord* rec;  // null -> raw int32 output
+    int32_t zp_a, zp_c;
+    int relu, rounding;
+    // F32 fast path (0 <= zp_c <= 255): clamp bounds before + zp_c and where
+    // zp_c is added (per byte, or once per packed word when the floor is 0)
+    int fast;
+    int debug_noepi;  // Q8G_CONV_NOEPI: skip the epilogue body (timing experiments only)
+    float lo, hi;
+    uint32_t zp1, zp4;
+    void* y;
+    unsigned long long* trace;  // debug (Q8G_TC_TRACE): CTA 0 per-unit stamps, else null
+};
+
+// CTA 0, local unit i < 64: [8192 + 64*which + i]; which: 0 halo issued,
+// 1 MMA start, 2 MMA committed, 3 epilogue start, 4 epilogue done; [8192+320]
+// = prologue done
+__device__ __forceinline__ void cv_stamp(const CvParams& p, int which, int i) {
+    if (p.trace && blockIdx.x == 0 && i < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8192 + which * 64 + i] = t;
+    }
+}
+
+__host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
+
+struct CvLayout {
+    int halo_off, halo_stride, b_off, wsum_off, corr_off, rec_off, soa_off, bar_off, tmemptr_off, total;
+};
+__host__ __device__ inline CvLayout cv_layout(const CvParams& p) {
+    CvLayout L;
+    L.halo_off = 1024;  // front guard (windows may start one position early)
+    L.halo_stride = align_up(p.halo_bytes + 2048, 1024);
+    L.b_off = L.halo_off + NBUF * L.halo_stride;
+    // B: [tap][kstep j][half][nq rows][16 B]
+    const int ksteps = p.planes / 2;
+    L.wsum_off = L.b_off + 9 * ksteps * 2 * p.nq * 16;
+    L.corr_off = L.wsum_off + 9 * p.oc_pad * 4;  // [9][oc_pad] tap weight sums
+    L.rec_off = L.corr_off + 16 * p.oc_pad * 4;  // [16][oc_pad]: c[n] + class correction
+    L.soa_off = L.rec_off + p.oc_pad * 16;       // [oc_pad] epilogue records (zp_b, mult)
+    L.bar_off = L.soa_off + p.oc_pad * 8;        // SoA: zp_b[oc_pad], mult_f32[oc_pad]
+    L.tmemptr_off = L.bar_off + (2 * NBUF + 5) * 8;  // + the operand-image barrier
+    L.total = L.tmemptr_off + 16 + 1024;
+    return L;
+}
+
+__device__ __forceinline__ uint64_t kmajor_noswz_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
+}
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+
+// packed weight element (k, n) (q8g_internal.cuh layout)
+__device__ __forceinline__ int8_t packed_at(const int8_t* pb, int np, int k, int n) {
+    const int kb = k / kKBlock, kin = k % kKBlock;
+    return pb[((size_t)kb * np + n) * kKBlock + (((kin / 16) ^ (n & 7)) * 16) + (kin % 16)];
+}
+
+// operand image: [tap][kstep j][half][nq rows][16 B] (rows < oc: weights of
+// input channels (2j+half)*16.., row oc_pad: all ones) then [9][oc_pad] sums
+__global__ void conv_prep_kernel(const CvParams p, uint8_t* img) {
+    const int ksteps = p.planes / 2;
+    const int nb = 9 * ksteps * 2 * p.nq;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb + 9 * p.oc_pad; idx += gridDim.x * blockDim.x) {
+        if (idx < nb) {
+            const int row = idx % p.nq, rest = idx / p.nq;  // rest = (t*ksteps + j)*2 + half
+            const int half = rest % 2, j = (rest / 2) % ksteps, t = rest / (2 * ksteps);
+            const int c0 = (2 * j + half) * 16;
+            uint32_t v[4] = {0, 0, 0, 0};
+            if (row < p.oc) {
+                for (int b = 0; b < 16; ++b)
+                    v[b / 4] |= (uint32_t)(uint8_t)packed_at(p.pb, p.np, t * p.c + c0 + b, row) << (8 * (b % 4));
+            } else if (row == p.oc_pad) {
+                v[0] = v[1] = v[2] = v[3] = 0x01010101u;  // ones column: row sums
+            }
+            *reinterpret_cast<uint4*>(img + (size_t)idx * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+        } else {
+            const int e = idx - nb, t = e / p.oc_pad, n = e % p.oc_pad;
+            int32_t s = 0;
+            if (n < p.oc)
+                for (int c = 0; c < p.c; ++c) s += packed_at(p.pb, p.np, t * p.c + c, n);
+            reinterpret_cast<int32_t*>(img + (size_t)nb * 16)[e] = s;
+        }
+    }
+}
+
+template <int MODE, int KS>  // MODE 0 raw int32, 1 F32_RNE, 2 REF; KS = C / 32 K-steps per tap
+__global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
+    conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const CvParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    const uint32_t base = (raw_addr + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base - raw_addr);
+    const CvLayout L = cv_layout(p);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t bar0 = base + L.bar_off;
+    auto full_bar = [&](int b) { return bar0 + 8u * b; };
+    auto empty_bar = [&](int b) { return bar0 + 8u * (NBUF + b); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + 2 + a); };
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmemptr_off);
+    const int ksteps = p.planes / 2;
+
+    // ---- B = [weights | ones] image + tap weight sums: one bulk copy of the
+    // per-weight operand image (built once, conv_prep_kernel)
+    const uint32_t img_bar = bar0 + 8u * (2 * NBUF + 4);
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(img_bar, 1);
+        ptx::fence_mbar_init();
+        ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
+        ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
+    }
+    for (int i = threadIdx.x; i < L.b_off / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);  // finite guards
+    __syncthreads();
+    ptx::mbar_wait(img_bar, 0);
+    const int32_t* wsum = reinterpret_cast<const int32_t*>(smem + L.wsum_off);
+    int32_t* corr = reinterpret_cast<int32_t*>(smem + L.corr_off);
+    for (int idx = threadIdx.x; idx < 16 * p.oc_pad; idx += blockDim.x) {
+        const int cls = idx / p.oc_pad, n = idx % p.oc_pad;
+        int64_t s = 0;
+        if (cls != 0 && n < p.oc) {
+            const int32_t zpb = MODE == 0 ? 0 : p.rec[n].zpb;
+            for (int t = 0; t < 9; ++t) {
+                const int kh = t / 3, kw = t % 3;
+                const bool padded = ((cls & 1) && kh == 0) || ((cls & 2) && kh == 2) || ((cls & 4) && kw == 0) ||
+                                    ((cls & 8) && kw == 2);
+                if (padded) s += (int64_t)wsum[t * p.oc_pad + n] - (int64_t)p.c * zpb;
+            }
+        }
+        // requant: the folded column constant c[n] joins the class correction
+        const int32_t c_n = (MODE == 0 || n >= p.oc) ? 0 : p.rec[n].c;
+        corr[idx] = (int32_t)((uint32_t)(uint64_t)(s * p.zp_a) + (uint32_t)c_n);
+    }
+    if (MODE != 0)
+        for (int n = threadIdx.x; n < p.oc_pad; n += blockDim.x) {
+            const int4 r4 = n < p.oc ? __ldg(reinterpret_cast<const int4*>(p.rec + n)) : make_int4(0, 0, 0, 0);
+            reinterpret_cast<int4*>(smem + L.rec_off)[n] = r4;
+            // SoA copies for the vectorised F32 epilogue
+            reinterpret_cast<int32_t*>(smem + L.soa_off)[n] = r4.y;                // zp_b
+            reinterpret_cast<int32_t*>(smem + L.soa_off)[p.oc_pad + n] = r4.z;     // fp32 multiplier bits
+        }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_x);
+        for (int b = 0; b < NBUF; ++b) {
+            ptx::mbar_init(full_bar(b), 1);
+            ptx::mbar_init(empty_bar(b), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull_bar(a), 1);
+            ptx::mbar_init(tempty_bar(a), 4);  // the 4 warps of the buffer's warpgroup
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_ptr;
+    if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8192 + 320] = t;
+    }
+
+    if (warp == 0) {
+        // ------------------------------------------------ halo producer
+        int b = 0;
+        uint32_t ph = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const int n = u / p.rblocks, rb = u % p.rblocks;
+            ptx::mbar_wait(empty_bar(b), ph ^ 1);
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(full_bar(b), (uint32_t)(p.planes * (ROWS + 2) * p.wp * 16));
+                const uint32_t dst = base + L.halo_off + b * L.halo_stride;
+                for (int q = 0; q < p.planes; ++q)
+                    tma_load_4d(dst + q * p.plane_bytes, &tmap_x, q * 16, -1, rb * ROWS - 1, n, full_bar(b));
+                cv_stamp(p, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
+            }
+            __syncwarp();
+            if (++b == NBUF) {
+                b = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        // descriptor templates computed once: the issue loop is then one add
+        // + one tcgen05.mma per K-step (the warp shares its SMSP with epilogue
+        // warps, so per-MMA integer work directly slows the tensor pipe)
+        const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(p.nq >> 3) << 17) | ((128u >> 4) << 24);
+        uint64_t a_t[9 * KS], b_t[9 * KS];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int sh1 = (t / 3) * p.wp + (t % 3);  // tap shift + 1 (non-negative)
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {
+                a_t[t * KS + j] = kmajor_noswz_desc((uint32_t)(2 * j * p.plane_bytes + sh1 * 16), (uint32_t)p.plane_bytes, 128);
+                b_t[t * KS + j] = kmajor_noswz_desc(base + L.b_off + (uint32_t)(((t * KS + j) * 2) * p.nq * 16),
+                                                    (uint32_t)(p.nq * 16), 128);
+            }
+        }
+        int b = 0, acc = 0;
+        uint32_t ph = 0, aph = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
+            ptx::mbar_wait(full_bar(b), ph);
+            ptx::tc_fence_after();
+            // start-address field (16-byte units) of halo position -1
+            const uint64_t halo16 = ((base + L.halo_off + b * L.halo_stride) >> 4) - 1;
+            const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+            if (ptx::elect_one()) {
+                cv_stamp(p, 1, (u - (int)blockIdx.x) / (int)gridDim.x);
+#pragma unroll
+                for (int i = 0; i < 9 * KS; ++i) ptx::mma_i8(d, a_t[i] + halo16, b_t[i], idesc, i != 0);
+                ptx::tc_commit(empty_bar(b));
+                ptx::tc_commit(tfull_bar(acc));
+                cv_stamp(p, 2, (u - (int)blockIdx.x) / (int)gridDim.x);
+            }
+            __syncwarp();
+            if (++b == NBUF) {
+                b = 0;
+                ph ^= 1;
+            }
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue
+        // warpgroup wg (warps 4-7 / 8-11) owns TMEM buffer wg = every other unit
+        const int wg = (warp - 4) / 4;
+        const int quarter = warp % 4;
+        const int r = quarter * 32 + lane;  // position within the unit's tile
+        const int orow = r / p.wp, ocol = r % p.wp - 1;
+        const int4* rec_s = reinterpret_cast<const int4*>(smem + L.rec_off);
+        uint32_t aph = 0;
+        int i = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++i) {
+            if ((i & 1) != wg) continue;
+            const int acc = wg;
+            const int n = u / p.rblocks, rb = u % p.rblocks;
+            const int oh = rb * ROWS + orow;
+            const bool valid = orow < ROWS && oh < p.h && ocol >= 0 && ocol < p.w;
+            const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
+            ptx::mbar_wait(tfull_bar(acc), aph);
+            ptx::tc_fence_after();
+            if (quarter == 0 && lane == 0) cv_stamp(p, 3, i);
+            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
+            const size_t pix = ((size_t)n * p.h + oh) * p.w + ocol;
+            int32_t rowsum = 0;
+            for (int ch0 = 0; ch0 < (p.debug_noepi ? 0 : p.oc_pad); ch0 += 64) {
+                // up to 64 columns (+ the row-sum column) in flight, one wait
+                uint32_t v4[4][16], rs[16];
+                const int nchunk = (p.oc_pad - ch0) >= 64 ? 4 : (p.oc_pad - ch0) / 16;
+                if (ch0 == 0) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)p.oc_pad, rs);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nchunk) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(ch0 + 16 * k), v4[k]);
+                ptx::tmem_ld_wait();
+                if (ch0 == 0) rowsum = (int32_t)rs[0];
+                if (ch0 == 0 && quarter == 0 && lane == 0 && p.trace && blockIdx.x == 0 && i < 64) {
+                    unsigned long long tt;  // debug: TMEM loads landed
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+                    p.trace[8192 + 384 + i] = tt;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k >= nchunk) break;
+                    const uint32_t (&v)[16] = v4[k];
+                    const int ch = ch0 + 16 * k;
+                    if (!valid) continue;
+                    const int32_t* crow = corr + cls * p.oc_pad + ch;
+                    if (MODE == 0) {
+                        int32_t* dst = reinterpret_cast<int32_t*>(p.y) + pix * p.oc + ch;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (ch + j < p.oc) dst[j] = (int32_t)(v[j] + (uint32_t)crow[j]);
+                        continue;
+                    }
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + pix * p.oc + ch;
+                    if (MODE == 1 && p.fast && ch + 16 <= p.oc && (p.oc % 16) == 0) {
+                        // F32_RNE fast path (0 <= zp_c <= 255): one RN conversion and
+                        // multiply, clamp in the pre-zp_c domain to integer bounds
+                        // (exact: rint is monotone), round via the 1.5*2^23 magic add;
+                        // with a zero clamp floor zp_c is added once per packed word
+                        const float magic = 12582912.0f;
+                        const int4* zq = reinterpret_cast<const int4*>(smem + L.soa_off) + ch / 4;
+                        const float4* mq = reinterpret_cast<const float4*>(smem + L.soa_off + p.oc_pad * 4) + ch / 4;
+                        const int4* cq = reinterpret_cast<const int4*>(crow);
+                        uint32_t w[4];
+#pragma unroll
+                        for (int g4 = 0; g4 < 4; ++g4) {
+                            const int4 zb = zq[g4];
+                            const float4 mm = mq[g4];
+                            const int4 cc = cq[g4];
+                            const int32_t zbv[4] = {zb.x, zb.y, zb.z, zb.w};
+                            const float mv[4] = {mm.x, mm.y, mm.z, mm.w};
+                            const int32_t cv[4] = {cc.x, cc.y, cc.z, cc.w};
+                            uint32_t b[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int32_t adj =
+                                    (int32_t)(v[g4 * 4 + k] - (uint32_t)zbv[k] * (uint32_t)rowsum + (uint32_t)cv[k]);
+                                float x = __fmul_rn(__int2float_rn(adj), mv[k]);
+                                x = fminf(fmaxf(x, p.lo), p.hi);
+                                b[k] = (uint32_t)__float_as_int(__fadd_rn(x, magic)) + p.zp1;
+                            }
+                            w[g4] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040),
+                                                0x5410) + p.zp4;
+                        }
+                        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                        continue;
+                    }
+                    uint32_t q[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int4 r4 = rec_s[ch + j];
+                        EpiRecord rc;
+                        rc.c = crow[j];  // c[n] + class correction
+                        rc.zpb = r4.y;
+                        const int32_t adj = adjust((int32_t)v[j], rowsum, rc);
+                        q[j] = MODE == 1 ? requant_f32(adj, __int_as_float(r4.z), p.zp_c, p.relu)
+                                         : requant_ref(adj, __hiloint2double(r4.w, r4.z), p.zp_c, p.relu);
+                    }
+                    if (ch + 16 <= p.oc && (p.oc % 16) == 0) {
+                        uint4 o;
+                        o.x = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+                        o.y = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+                        o.z = q[8] | (q[9] << 8) | (q[10] << 16) | (q[11] << 24);
+                        o.w = q[12] | (q[13] << 8) | (q[14] << 16) | (q[15] << 24);
+                        *reinterpret_cast<uint4*>(dst) = o;
+                    } else {
+                        for (int j = 0; j < 16; ++j)
+                            if (ch + j < p.oc) dst[j] = (uint8_t)q[j];
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+            if (quarter == 0 && lane == 0) cv_stamp(p, 4, i);
+            aph ^= 1;
+        }
+    }
+
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem_base);
+    }
+}
+
+CvParams make_params(const ConvArgs& a) {
+    CvParams p{};
+    p.nb = a.nb;
+    p.h = a.h;
+    p.w = a.w;
+    p.c = a.c;
+    p.oc = a.pw->n;
+    p.wp = a.w + 2;
+    p.planes = a.c / 16;
+    p.oc_pad = align_up(p.oc, 16);
+    p.nq = p.oc_pad + 16;
+    p.rblocks = (a.h + ROWS - 1) / ROWS;
+    p.units = a.nb * p.rblocks;
+    p.plane_bytes = align_up((ROWS + 2) * p.wp * 16, 128);
+    p.halo_bytes = p.planes * p.plane_bytes;
+    p.pb = a.pw->data;
+    p.np = a.pw->np;
+    p.img = a.pw->conv_img;
+    p.img_bytes = 9 * (p.planes / 2) * 2 * p.nq * 16 + 9 * p.oc_pad * 4;
+    p.rec = a.raw ? nullptr : a.ep->rec;
+    p.zp_a = a.zp_a;
+    p.zp_c = a.raw ? 0 : a.ep->zp_c;
+    p.relu = a.raw ? 0 : a.ep->relu;
+    p.rounding = a.raw ? 0 : a.ep->rounding;
+    p.fast = (!a.raw && p.zp_c >= 0 && p.zp_c <= 255) ? 1 : 0;
+    p.debug_noepi = getenv("Q8G_CONV_NOEPI") != nullptr;
+    p.lo = p.relu ? 0.0f : (float)(-p.zp_c);
+    p.hi = (float)(255 - p.zp_c);
+    p.zp1 = p.relu ? 0u : (uint32_t)p.zp_c;
+    p.zp4 = p.relu ? (uint32_t)p.zp_c * 0x01010101u : 0u;
+    p.y = a.y;
+    p.trace = tc_trace_buffer_ptr();
+    return p;
+}
+
+}  // namespace
+
+bool conv_tc_supported(const ConvArgs& a) {
+    if (tmap_encoder() == nullptr) return false;
+    if (a.c % 32 != 0 || (a.c != 32 && a.c != 64 && a.c != 128) || a.pw->n > 240 || a.w + 2 > 256) return false;
+    if (ROWS * (a.w + 2) > 128) return false;  // one M tile per unit
+    const CvParams p = make_params(a);
+    if (p.nq * 2 > 512 || p.nq > 256) return false;
+    return cv_layout(p).total <= 232448;
+}
+
+cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
+    auto enc = tmap_encoder();
+    CvParams p = make_params(a);
+    CUtensorMap tmap;
+    cuuint64_t dims[4] = {(cuuint64_t)a.c, (cuuint64_t)a.w, (cuuint64_t)a.h, (cuuint64_t)a.nb};
+    cuuint64_t strides[3] = {(cuuint64_t)a.c, (cuuint64_t)a.w * a.c, (cuuint64_t)a.h * a.w * a.c};
+    cuuint32_t box[4] = {16, (cuuint32_t)(a.w + 2), (cuuint32_t)(ROWS + 2), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(a.x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    const CvLayout L = cv_layout(p);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // per-weight operand image, built once per (weight, C) on first use (the
+    // first conv call on a weight must not be inside a stream capture)
+    auto* pw = const_cast<q8g_packed_b*>(a.pw);
+    if (pw->conv_img_c != a.c) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+        if (pw->conv_img) cudaFree(pw->conv_img);
+        pw->conv_img = nullptr;
+        pw->conv_img_c = 0;
+        cudaError_t e = cudaMalloc(&pw->conv_img, (size_t)p.img_bytes);
+        if (e != cudaSuccess) return e;
+        conv_prep_kernel<<<64, 256, 0, s>>>(p, pw->conv_img);
+        count_launch(kFamPack);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        pw->conv_img_c = a.c;
+        pw->conv_img_bytes = (size_t)p.img_bytes;
+    }
+    p.img = pw->conv_img;
+    int grid = sm_count(dev);
+    if (grid > p.units) grid = p.units;
+    const int mode = a.raw ? 0 : (a.ep->rounding == Q8G_ROUND_F32_RNE ? 1 : 2);
+    const int ks = a.c / 32;
+    const int threads = 128 + 32 * EPI_WARPS;
+    auto go = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e == cudaSuccess) kern<<<grid, threads, L.total, s>>>(tmap, p);
+        return e;
+    };
+    cudaError_t e;
+#define Q8G_CONV_KS(M)                                           \
+    (ks == 1 ? go(conv3x3_tc_kernel<M, 1>) : ks == 2 ? go(conv3x3_tc_kernel<M, 2>) \
+             : ks == 4 ? go(conv3x3_tc_kernel<M, 4>) : cudaErrorNotSupported)
+    if (mode == 0)
+        e = Q8G_CONV_KS(0);
+    else if (mode == 1)
+        e = Q8G_CONV_KS(1);
+    else
+        e = Q8G_CONV_KS(2);
+#undef Q8G_CONV_KS
+    if (e != cudaSuccess) return e;
+    count_launch(kFamConvTc);
+    return cudaGetLastError();
+}
+
+}  // namespace q8g

@@ -92,6 +92,11 @@ struct q8g_packed_b {
     int8_t* data = nullptr;       // device, kp*np bytes
     int32_t* colsum_dev = nullptr; // device, np entries (zero beyond n)
     int32_t* colsum_host = nullptr;
+    // conv3x3 tensor-core operand image (conv_tc.cu), built once per C:
+    // the smem B layout followed by the per-tap weight sums
+    uint8_t* conv_img = nullptr;
+    int conv_img_c = 0;
+    size_t conv_img_bytes = 0;
 };
 
 struct q8g_epilogue {
@@ -184,6 +189,8 @@ struct ConvArgs {
     bool raw;
 };
 cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s);
+bool conv_tc_supported(const ConvArgs& a);
+cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s);
 
 cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c,
                              const q8g_dw_filter* f, uint8_t* y, cudaStream_t s);

@@ -33,7 +33,8 @@ def conv_oracle(orc, cc: configs.ConvCase):
     return acc, out
 
 
-@pytest.mark.parametrize("shape", [(1, 5, 7, 4, 8), (2, 9, 9, 16, 24), (3, 14, 14, 64, 64), (1, 3, 3, 3, 5)])
+@pytest.mark.parametrize("shape", [(1, 5, 7, 4, 8), (2, 9, 9, 16, 24), (3, 14, 14, 64, 64), (1, 3, 3, 3, 5),
+                                   (2, 7, 9, 32, 40), (1, 1, 1, 64, 16), (2, 3, 60, 32, 64), (1, 6, 5, 128, 200)])
 def test_conv3x3_small_vs_oracle(cuda, orc, shape):
     nb, h, w, c, oc = shape
     cc = configs.conv_case(orc, nb, h, w, c, oc, seed=sum(shape))

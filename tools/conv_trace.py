@@ -1,0 +1,47 @@
+"""Per-unit timeline of CTA 0 in the tensor-core conv3x3 kernel (debug;
+Q8G_TC_TRACE=1), C3 shape.  Columns: halo issued / MMA start / MMA committed
+/ epilogue start / epilogue done, us from the first stamp; plus prologue end."""
+import ctypes as C
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+os.environ.setdefault("Q8G_TC_TRACE", "1")
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2101_05615_b200 as q8  # noqa: E402
+from paper_2101_05615_b200 import _lib  # noqa: E402
+
+
+def main():
+    nb, h, w, c, oc = 32, 56, 56, 64, 64
+    rng = np.random.default_rng(0)
+    wt = rng.integers(-128, 128, (3, 3, c, oc)).astype(np.int8)
+    pw = q8.prepack_conv3x3_weights(wt)
+    rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=9 * c, bias=rng.integers(-1000, 1001, oc).astype(np.int32),
+                          zp_b_per_channel=rng.integers(-10, 11, oc).astype(np.int32),
+                          multiplier_f32_per_channel=np.full(oc, 0.0005, np.float32), rounding=q8.ROUND_F32_RNE)
+    pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
+    x = torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device="cuda")
+    y = torch.empty((nb, h, w, oc), dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        q8.execute_conv3x3(x, pw, y, pipe)
+    torch.cuda.synchronize()
+    buf = (C.c_uint64 * (8 * 1024 + 512))()
+    _lib.load().q8g_debug_tc_trace(buf, 2048)
+    a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+    units = a[8192:8192 + 320].reshape(5, 64)
+    t0 = min(units[0][units[0] > 0].min(), a[8192 + 320])
+    print(f"prologue done at {(a[8192 + 320] - t0) / 1e3:.2f} us (relative to first stamp)")
+    n = int((units[0] > 0).sum())
+    tl = a[8192 + 384:8192 + 448]
+    print("unit  halo_issued  mma_start  mma_commit  epi_start  epi_done  tmem_landed (us)")
+    for i in range(n):
+        print(f"{i:4d} " + " ".join(f"{(units[j, i] - t0) / 1e3:9.2f}" for j in range(5)) +
+              f" {(tl[i] - t0) / 1e3:9.2f}")
+
+
+if __name__ == "__main__":
+    main()
