@@ -67,7 +67,9 @@ uint64_t q8g_launch_count(void);
  * [6] depthwise CUDA-core, [7] depthwise tcgen05 */
 int q8g_launch_stats(uint64_t* counts, int n);
 /* debug (env Q8G_TC_TRACE set): 8 globaltimer stamps per CTA of the last
- * tensor-core GEMM launch; returns the number of CTA records copied */
+ * tensor-core GEMM launch; returns the number of CTA records copied.  With
+ * max_ctas > 1024 the whole 10240-word trace buffer is copied (out must hold
+ * 10240 words): + per-unit stamps of CTA 0 and per-CTA conv entry/exit */
 int q8g_debug_tc_trace(uint64_t* out, int max_ctas);
 
 /* ---- blocking (dispatch.hpp:17-30, pack.hpp:24-37) ---- */

@@ -47,6 +47,14 @@ int sm_count(int device) {
     return v;
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("Q8G_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static int validate_blocking(const q8g_blocking& bp) {
     if (bp.mcb < 1 || bp.ncb < 1 || bp.kcb < 1 || bp.mr < 1 || bp.nr < 1)
         return fail(Q8G_EINVAL, "BlockingParams: all sizes must be >= 1");

@@ -7,12 +7,13 @@
 // K = 9C x N = OC matrix, epilogue table from q8g_epilogue_create (K = 9C).
 //
 // Design: im2col is never materialised.  A work unit is (image, ROWS output
-// rows); TMA loads a halo of ROWS+2 input rows x (W+2) padded positions,
-// stored as C/16 planes of 16 channels (16 B per position), out-of-range
-// taps zero-filled.  For tap t and channel pair-of-planes j the MMA A
-// operand is the window starting at position q + (t/3)*(W+2) + t%3 - 1 of
-// planes 2j, 2j+1: a SWIZZLE_NONE K-major descriptor with LBO = the plane
-// distance.  B (built once per CTA in smem from the packed weights) has the
+// rows); one TMA loads a halo of ROWS+2 input rows x (W+2) padded positions
+// x C channels in natural NHWC order (rows of C bytes, hardware swizzle of
+// span C = 32/64/128), out-of-range taps zero-filled.  For tap t and K-step
+// j (32 channels) the MMA A operand is the window starting at position
+// q + (t/3)*(W+2) + t%3 - 1, bytes 32j.. of each row: a swizzled K-major
+// descriptor whose start may sit at any row because the tensor core applies
+// the swizzle on absolute smem addresses.  B (per-weight operand image) has the
 // OC output channels plus one all-ones column, so the tensor core also
 // produces the row sum of the zero-filled A.  The exact correction for
 // zero- instead of zp_a-padding depends only on which taps of a pixel are
@@ -22,6 +23,10 @@
 // and adj = D[j] - zp_b[j] * D[ones] + c[j] + corr[cls][j].
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "ptx.cuh"
 #include "q8g_internal.cuh"
@@ -35,8 +40,9 @@ unsigned long long* tc_trace_buffer_ptr();
 namespace {
 
 constexpr int ROWS = 2;      // output rows per unit (ROWS * (W+2) <= 128 -> one M tile)
-constexpr int NBUF = 3;      // halo buffers in flight
-constexpr int EPI_WARPS = 8;  // two warpgroups, one per TMEM accumulator buffer
+constexpr int MAX_BUF = 8;   // halo buffers in flight: p.nbuf <= MAX_BUF, as many as fit in smem
+constexpr int EPI_WARPS = 8;  // two warpgroups; warpgroup g takes every other unit
+constexpr int MAX_ACC = 4;    // TMEM accumulators (nacc = 4 when nq <= 128, else 2)
 
 struct CvParams {
     int nb, h, w, c, oc;
@@ -45,8 +51,9 @@ struct CvParams {
     int nq;            // MMA N = round_up(oc, 16) + 16 (ones column at index oc_pad)
     int oc_pad;        // round_up(oc, 16)
     int rblocks, units;
-    int plane_bytes;   // (ROWS+2) * wp * 16, padded to 128
-    int halo_bytes;    // planes * plane_bytes
+    int nacc, acc_cols;  // TMEM accumulators in flight and their column stride
+    int nbuf;            // halo buffers
+    int halo_bytes;      // (ROWS+2) * wp * C
     const int8_t* pb;  // packed weights
     int np;            // packed N pad
     const uint8_t* img;  // operand image: smem B layout + [9][oc_pad] tap sums
@@ -54,24 +61,30 @@ struct CvParams {
     const EpiRecord* rec;  // null -> raw int32 output
     int32_t zp_a, zp_c;
     int relu, rounding;
-    // F32 fast path (0 <= zp_c <= 255): clamp bounds before + zp_c and where
-    // zp_c is added (per byte, or once per packed word when the floor is 0)
-    int fast;
-    int debug_noepi;  // Q8G_CONV_NOEPI: skip the epilogue body (timing experiments only)
-    float lo, hi;
-    uint32_t zp1, zp4;
+    int fast;         // F32 fast path (0 <= zp_c <= 255, epi_f32_fast)
+    int debug;        // Q8G_CONV_DEBUG bits (timing experiments only): 1 skip epilogue body, 2 skip MMAs, 4 one MMA per unit, 8 no tcgen05 fence in the MMA loop
     void* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): CTA 0 per-unit stamps, else null
 };
 
 // CTA 0, local unit i < 64: [8192 + 64*which + i]; which: 0 halo issued,
-// 1 MMA start, 2 MMA committed, 3 epilogue start, 4 epilogue done; [8192+320]
-// = prologue done
+// 1 MMA start, 2 MMA committed, 3 epilogue start, 4 epilogue done, [9216 + 64*(which-5) + i]:
+// 5 MMA warp past tempty, 6 past full; [8192+320]
+// = prologue done, [8192+321] = kernel entry
 __device__ __forceinline__ void cv_stamp(const CvParams& p, int which, int i) {
     if (p.trace && blockIdx.x == 0 && i < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[8192 + which * 64 + i] = t;
+        p.trace[which < 5 ? 8192 + which * 64 + i : 9216 + (which - 5) * 64 + i] = t;
+    }
+}
+
+// CTA 0 prologue stamps [9344 + k]: 0 barriers/image issued, 1 guards zeroed, 2 TMEM allocated
+__device__ __forceinline__ void cv_pstamp(const CvParams& p, int k) {
+    if (p.trace && blockIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[9344 + k] = t;
     }
 }
 
@@ -84,7 +97,7 @@ __host__ __device__ inline CvLayout cv_layout(const CvParams& p) {
     CvLayout L;
     L.halo_off = 1024;  // front guard (windows may start one position early)
     L.halo_stride = align_up(p.halo_bytes + 2048, 1024);
-    L.b_off = L.halo_off + NBUF * L.halo_stride;
+    L.b_off = L.halo_off + p.nbuf * L.halo_stride;
     // B: [tap][kstep j][half][nq rows][16 B]
     const int ksteps = p.planes / 2;
     L.wsum_off = L.b_off + 9 * ksteps * 2 * p.nq * 16;
@@ -92,9 +105,19 @@ __host__ __device__ inline CvLayout cv_layout(const CvParams& p) {
     L.rec_off = L.corr_off + 16 * p.oc_pad * 4;  // [16][oc_pad]: c[n] + class correction
     L.soa_off = L.rec_off + p.oc_pad * 16;       // [oc_pad] epilogue records (zp_b, mult)
     L.bar_off = L.soa_off + p.oc_pad * 8;        // SoA: zp_b[oc_pad], mult_f32[oc_pad]
-    L.tmemptr_off = L.bar_off + (2 * NBUF + 5) * 8;  // + the operand-image barrier
+    L.tmemptr_off = L.bar_off + (2 * MAX_BUF + 2 * MAX_ACC + 1) * 8;  // + the operand-image barrier
     L.total = L.tmemptr_off + 16 + 1024;
     return L;
+}
+
+// K-major operand with rows of S = 32/64/128 bytes in the matching hardware
+// swizzle (8-row groups of 8*S bytes).  The tensor core applies the XOR on
+// absolute smem address bits, as TMA writes it, so the start may sit at any
+// row (tap-shifted windows) with base_offset 0 (verified: tools/swz_test.cu)
+__host__ __device__ inline uint64_t kmajor_swz_desc(uint32_t addr, int S) {
+    const uint64_t code = S == 128 ? 2 : S == 64 ? 4 : 6;
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)((8 * S) >> 4) << 32) |
+           ((uint64_t)1 << 46) | (code << 61);
 }
 
 __device__ __forceinline__ uint64_t kmajor_noswz_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -144,6 +167,49 @@ __global__ void conv_prep_kernel(const CvParams p, uint8_t* img) {
     }
 }
 
+// d = {c[15:0], sat_u8(a), sat_u8(b)} (one I2IP)
+__device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// F32_RNE requant of NCH x 16 accumulator columns of one position, straight
+// line (one basic block for the scheduler).  Per output: adj = D + c + (-zp_b)
+// * rowsum (wrapping), x = RN(float(adj) * m), then the magic add
+// y = x + 1.5*2^23 gives bits(y) - 0x4B400000 = rint(x) for |x| <= 2^22 and
+// stays monotone beyond (for x >= -2^23, the floor applied here, or 0 under
+// ReLU), so the saturating u8 pack of bits(y) - (0x4B400000 - zp_c) is exactly
+// clamp(rint(x) + zp_c, relu ? zp_c : 0, 255) (requant.cuh requant_f32).
+template <bool RELU, int NCH>
+__device__ __forceinline__ void epi_f32_fast(const uint32_t (&v)[4][16], int32_t rowsum, const int4* nzq,
+                                             const float4* mq, const int4* cq, int32_t zoff, uint4* dst,
+                                             bool valid) {
+    uint32_t w[4 * NCH];
+#pragma unroll
+    for (int g = 0; g < 4 * NCH; ++g) {
+        const int4 zb = nzq[g];
+        const float4 mm = mq[g];
+        const int4 cc = cq[g];
+        const int32_t zv[4] = {zb.x, zb.y, zb.z, zb.w};
+        const float mv[4] = {mm.x, mm.y, mm.z, mm.w};
+        const int32_t cv[4] = {cc.x, cc.y, cc.z, cc.w};
+        int32_t r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t adj = (int32_t)(v[g / 4][(g % 4) * 4 + k] + ((uint32_t)cv[k] + (uint32_t)zv[k] * (uint32_t)rowsum));
+            float x = __fmul_rn(__int2float_rn(adj), mv[k]);
+            x = fmaxf(x, RELU ? 0.0f : -8388608.0f);
+            r[k] = __float_as_int(__fadd_rn(x, 12582912.0f)) - zoff;
+        }
+        w[g] = pack_sat_u8(r[1], r[0], pack_sat_u8(r[3], r[2], 0u));
+    }
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+    }
+}
+
 template <int MODE, int KS>  // MODE 0 raw int32, 1 F32_RNE, 2 REF; KS = C / 32 K-steps per tap
 __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const CvParams p) {
@@ -155,70 +221,57 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t bar0 = base + L.bar_off;
     auto full_bar = [&](int b) { return bar0 + 8u * b; };
-    auto empty_bar = [&](int b) { return bar0 + 8u * (NBUF + b); };
-    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + 2 + a); };
+    auto empty_bar = [&](int b) { return bar0 + 8u * (MAX_BUF + b); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * MAX_BUF + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * MAX_BUF + MAX_ACC + a); };
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmemptr_off);
-    const int ksteps = p.planes / 2;
+    const uint32_t img_bar = bar0 + 8u * (2 * MAX_BUF + 2 * MAX_ACC);
+    ptx::griddep_launch_dependents();
+    if (threadIdx.x == 0 && p.trace && blockIdx.x < 160) {  // per-CTA entry stamp
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (blockIdx.x == 0) p.trace[8192 + 321] = t;
+        p.trace[8704 + blockIdx.x] = t;
+    }
 
-    // ---- B = [weights | ones] image + tap weight sums: one bulk copy of the
-    // per-weight operand image (built once, conv_prep_kernel)
-    const uint32_t img_bar = bar0 + 8u * (2 * NBUF + 4);
+    // ---- barriers first, then everything overlaps: the producer streams
+    // halos while the operand image (B = [weights | ones] + tap weight sums,
+    // built once per weight by conv_prep_kernel) lands and the epilogue
+    // warps build their correction tables
     if (threadIdx.x == 0) {
-        ptx::mbar_init(img_bar, 1);
-        ptx::fence_mbar_init();
-        ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
-        ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
-    }
-    for (int i = threadIdx.x; i < L.b_off / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);  // finite guards
-    __syncthreads();
-    ptx::mbar_wait(img_bar, 0);
-    const int32_t* wsum = reinterpret_cast<const int32_t*>(smem + L.wsum_off);
-    int32_t* corr = reinterpret_cast<int32_t*>(smem + L.corr_off);
-    for (int idx = threadIdx.x; idx < 16 * p.oc_pad; idx += blockDim.x) {
-        const int cls = idx / p.oc_pad, n = idx % p.oc_pad;
-        int64_t s = 0;
-        if (cls != 0 && n < p.oc) {
-            const int32_t zpb = MODE == 0 ? 0 : p.rec[n].zpb;
-            for (int t = 0; t < 9; ++t) {
-                const int kh = t / 3, kw = t % 3;
-                const bool padded = ((cls & 1) && kh == 0) || ((cls & 2) && kh == 2) || ((cls & 4) && kw == 0) ||
-                                    ((cls & 8) && kw == 2);
-                if (padded) s += (int64_t)wsum[t * p.oc_pad + n] - (int64_t)p.c * zpb;
-            }
-        }
-        // requant: the folded column constant c[n] joins the class correction
-        const int32_t c_n = (MODE == 0 || n >= p.oc) ? 0 : p.rec[n].c;
-        corr[idx] = (int32_t)((uint32_t)(uint64_t)(s * p.zp_a) + (uint32_t)c_n);
-    }
-    if (MODE != 0)
-        for (int n = threadIdx.x; n < p.oc_pad; n += blockDim.x) {
-            const int4 r4 = n < p.oc ? __ldg(reinterpret_cast<const int4*>(p.rec + n)) : make_int4(0, 0, 0, 0);
-            reinterpret_cast<int4*>(smem + L.rec_off)[n] = r4;
-            // SoA copies for the vectorised F32 epilogue
-            reinterpret_cast<int32_t*>(smem + L.soa_off)[n] = r4.y;                // zp_b
-            reinterpret_cast<int32_t*>(smem + L.soa_off)[p.oc_pad + n] = r4.z;     // fp32 multiplier bits
-        }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-
-    if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_x);
-        for (int b = 0; b < NBUF; ++b) {
+        ptx::mbar_init(img_bar, 1);
+        for (int b = 0; b < p.nbuf; ++b) {
             ptx::mbar_init(full_bar(b), 1);
             ptx::mbar_init(empty_bar(b), 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < MAX_ACC; ++a) {
             ptx::mbar_init(tfull_bar(a), 1);
-            ptx::mbar_init(tempty_bar(a), 4);  // the 4 warps of the buffer's warpgroup
+            ptx::mbar_init(tempty_bar(a), 4);  // the 4 warps of the unit's warpgroup
         }
         ptx::fence_mbar_init();
+        ptx::griddep_wait();  // PDL: the operand image may come from the preceding grid
+        ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
+        ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
+        cv_pstamp(p, 0);
     }
-    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+    // halo guard bands (windows start one position early / run past the end)
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) reinterpret_cast<uint4*>(smem + L.halo_off - 1024)[i] = make_uint4(0, 0, 0, 0);
+    for (int b = 0; b < p.nbuf; ++b) {
+        uint4* g = reinterpret_cast<uint4*>(smem + L.halo_off + b * L.halo_stride + p.halo_bytes);
+        for (int i = threadIdx.x; i < (L.halo_stride - p.halo_bytes) / 16; i += blockDim.x) g[i] = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) cv_pstamp(p, 1);
+    if (warp == 2) {
+        ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+        if (lane == 0) cv_pstamp(p, 2);
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
+    ptx::griddep_wait();  // PDL: inputs / outputs are touched only after the previous grid
     if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -233,14 +286,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             const int n = u / p.rblocks, rb = u % p.rblocks;
             ptx::mbar_wait(empty_bar(b), ph ^ 1);
             if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(full_bar(b), (uint32_t)(p.planes * (ROWS + 2) * p.wp * 16));
-                const uint32_t dst = base + L.halo_off + b * L.halo_stride;
-                for (int q = 0; q < p.planes; ++q)
-                    tma_load_4d(dst + q * p.plane_bytes, &tmap_x, q * 16, -1, rb * ROWS - 1, n, full_bar(b));
+                // one 4D TMA: (ROWS+2) rows x (W+2) positions x C bytes, natural
+                // NHWC order, hardware swizzle of span C, out-of-image taps zero
+                ptx::mbar_arrive_expect_tx(full_bar(b), (uint32_t)p.halo_bytes);
+                tma_load_4d(base + L.halo_off + b * L.halo_stride, &tmap_x, 0, -1, rb * ROWS - 1, n, full_bar(b));
                 cv_stamp(p, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
             }
             __syncwarp();
-            if (++b == NBUF) {
+            if (++b == p.nbuf) {
                 b = 0;
                 ph ^= 1;
             }
@@ -257,34 +310,38 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             const int sh1 = (t / 3) * p.wp + (t % 3);  // tap shift + 1 (non-negative)
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
-                a_t[t * KS + j] = kmajor_noswz_desc((uint32_t)(2 * j * p.plane_bytes + sh1 * 16), (uint32_t)p.plane_bytes, 128);
+                a_t[t * KS + j] = kmajor_swz_desc((uint32_t)(sh1 * p.c + j * 32), p.c);
                 b_t[t * KS + j] = kmajor_noswz_desc(base + L.b_off + (uint32_t)(((t * KS + j) * 2) * p.nq * 16),
                                                     (uint32_t)(p.nq * 16), 128);
             }
         }
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
+        ptx::mbar_wait(img_bar, 0);
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
+            if (lane == 0) cv_stamp(p, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
             ptx::mbar_wait(full_bar(b), ph);
-            ptx::tc_fence_after();
+            if (lane == 0) cv_stamp(p, 6, (u - (int)blockIdx.x) / (int)gridDim.x);
+            if (!(p.debug & 8)) ptx::tc_fence_after();
             // start-address field (16-byte units) of halo position -1
-            const uint64_t halo16 = ((base + L.halo_off + b * L.halo_stride) >> 4) - 1;
-            const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+            const uint64_t halo16 = (base + L.halo_off + b * L.halo_stride - (uint32_t)p.c) >> 4;
+            const uint32_t d = tmem_base + (uint32_t)(acc * p.acc_cols);
             if (ptx::elect_one()) {
                 cv_stamp(p, 1, (u - (int)blockIdx.x) / (int)gridDim.x);
 #pragma unroll
-                for (int i = 0; i < 9 * KS; ++i) ptx::mma_i8(d, a_t[i] + halo16, b_t[i], idesc, i != 0);
+                for (int i = 0; i < 9 * KS; ++i)
+                    if (!(p.debug & 2) && (!(p.debug & 4) || i == 0)) ptx::mma_i8(d, a_t[i] + halo16, b_t[i], idesc, i != 0);
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
                 cv_stamp(p, 2, (u - (int)blockIdx.x) / (int)gridDim.x);
             }
             __syncwarp();
-            if (++b == NBUF) {
+            if (++b == p.nbuf) {
                 b = 0;
                 ph ^= 1;
             }
-            if (++acc == 2) {
+            if (++acc == p.nacc) {
                 acc = 0;
                 aph ^= 1;
             }
@@ -297,11 +354,43 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         const int r = quarter * 32 + lane;  // position within the unit's tile
         const int orow = r / p.wp, ocol = r % p.wp - 1;
         const int4* rec_s = reinterpret_cast<const int4*>(smem + L.rec_off);
-        uint32_t aph = 0;
+        const int32_t* corr = reinterpret_cast<const int32_t*>(smem + L.corr_off);
+        {
+            // per-CTA tables: corr[class][n] = c[n] + zp_a * sum over the
+            // class's padded taps of (tap weight sum - C*zp_b[n]); SoA copies
+            const int et = threadIdx.x - 128;
+            ptx::mbar_wait(img_bar, 0);
+            const int32_t* wsum = reinterpret_cast<const int32_t*>(smem + L.wsum_off);
+            int32_t* corr_w = reinterpret_cast<int32_t*>(smem + L.corr_off);
+            for (int idx = et; idx < 16 * p.oc_pad; idx += 32 * EPI_WARPS) {
+                const int cls = idx / p.oc_pad, n = idx % p.oc_pad;
+                int64_t s = 0;
+                if (cls != 0 && n < p.oc) {
+                    const int32_t zpb = MODE == 0 ? 0 : p.rec[n].zpb;
+                    for (int t = 0; t < 9; ++t) {
+                        const int kh = t / 3, kw = t % 3;
+                        const bool padded = ((cls & 1) && kh == 0) || ((cls & 2) && kh == 2) ||
+                                            ((cls & 4) && kw == 0) || ((cls & 8) && kw == 2);
+                        if (padded) s += (int64_t)wsum[t * p.oc_pad + n] - (int64_t)p.c * zpb;
+                    }
+                }
+                const int32_t c_n = (MODE == 0 || n >= p.oc) ? 0 : p.rec[n].c;
+                corr_w[idx] = (int32_t)((uint32_t)(uint64_t)(s * p.zp_a) + (uint32_t)c_n);
+            }
+            if (MODE != 0)
+                for (int n = et; n < p.oc_pad; n += 32 * EPI_WARPS) {
+                    const int4 r4 = n < p.oc ? __ldg(reinterpret_cast<const int4*>(p.rec + n)) : make_int4(0, 0, 0, 0);
+                    reinterpret_cast<int4*>(smem + L.rec_off)[n] = r4;
+                    reinterpret_cast<int32_t*>(smem + L.soa_off)[n] = (int32_t)(0u - (uint32_t)r4.y);  // -zp_b
+                    reinterpret_cast<int32_t*>(smem + L.soa_off)[p.oc_pad + n] = r4.z;  // fp32 multiplier bits
+                }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        }
         int i = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++i) {
             if ((i & 1) != wg) continue;
-            const int acc = wg;
+            const int acc = i % p.nacc;
+            const uint32_t aph = (uint32_t)(i / p.nacc) & 1u;
             const int n = u / p.rblocks, rb = u % p.rblocks;
             const int oh = rb * ROWS + orow;
             const bool valid = orow < ROWS && oh < p.h && ocol >= 0 && ocol < p.w;
@@ -309,10 +398,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
             if (quarter == 0 && lane == 0) cv_stamp(p, 3, i);
-            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
+            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.acc_cols);
             const size_t pix = ((size_t)n * p.h + oh) * p.w + ocol;
             int32_t rowsum = 0;
-            for (int ch0 = 0; ch0 < (p.debug_noepi ? 0 : p.oc_pad); ch0 += 64) {
+            for (int ch0 = 0; ch0 < ((p.debug & 1) ? 0 : p.oc_pad); ch0 += 64) {
                 // up to 64 columns (+ the row-sum column) in flight, one wait
                 uint32_t v4[4][16], rs[16];
                 const int nchunk = (p.oc_pad - ch0) >= 64 ? 4 : (p.oc_pad - ch0) / 16;
@@ -326,6 +415,24 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                     unsigned long long tt;  // debug: TMEM loads landed
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
                     p.trace[8192 + 384 + i] = tt;
+                }
+                if (MODE == 1 && p.fast && (p.oc % 16) == 0) {
+                    const int4* nzq = reinterpret_cast<const int4*>(smem + L.soa_off) + ch0 / 4;
+                    const float4* mq = reinterpret_cast<const float4*>(smem + L.soa_off + p.oc_pad * 4) + ch0 / 4;
+                    const int4* cq = reinterpret_cast<const int4*>(corr + cls * p.oc_pad + ch0);
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.y) + pix * p.oc + ch0);
+                    const int32_t zoff = 0x4B400000 - p.zp_c;
+#define Q8G_EPI_FAST(R)                                                                   \
+    (nchunk == 4   ? epi_f32_fast<R, 4>(v4, rowsum, nzq, mq, cq, zoff, dst, valid)     \
+     : nchunk == 3 ? epi_f32_fast<R, 3>(v4, rowsum, nzq, mq, cq, zoff, dst, valid)     \
+     : nchunk == 2 ? epi_f32_fast<R, 2>(v4, rowsum, nzq, mq, cq, zoff, dst, valid)     \
+                   : epi_f32_fast<R, 1>(v4, rowsum, nzq, mq, cq, zoff, dst, valid))
+                    if (p.relu)
+                        Q8G_EPI_FAST(true);
+                    else
+                        Q8G_EPI_FAST(false);
+#undef Q8G_EPI_FAST
+                    continue;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -342,39 +449,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                         continue;
                     }
                     uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + pix * p.oc + ch;
-                    if (MODE == 1 && p.fast && ch + 16 <= p.oc && (p.oc % 16) == 0) {
-                        // F32_RNE fast path (0 <= zp_c <= 255): one RN conversion and
-                        // multiply, clamp in the pre-zp_c domain to integer bounds
-                        // (exact: rint is monotone), round via the 1.5*2^23 magic add;
-                        // with a zero clamp floor zp_c is added once per packed word
-                        const float magic = 12582912.0f;
-                        const int4* zq = reinterpret_cast<const int4*>(smem + L.soa_off) + ch / 4;
-                        const float4* mq = reinterpret_cast<const float4*>(smem + L.soa_off + p.oc_pad * 4) + ch / 4;
-                        const int4* cq = reinterpret_cast<const int4*>(crow);
-                        uint32_t w[4];
-#pragma unroll
-                        for (int g4 = 0; g4 < 4; ++g4) {
-                            const int4 zb = zq[g4];
-                            const float4 mm = mq[g4];
-                            const int4 cc = cq[g4];
-                            const int32_t zbv[4] = {zb.x, zb.y, zb.z, zb.w};
-                            const float mv[4] = {mm.x, mm.y, mm.z, mm.w};
-                            const int32_t cv[4] = {cc.x, cc.y, cc.z, cc.w};
-                            uint32_t b[4];
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const int32_t adj =
-                                    (int32_t)(v[g4 * 4 + k] - (uint32_t)zbv[k] * (uint32_t)rowsum + (uint32_t)cv[k]);
-                                float x = __fmul_rn(__int2float_rn(adj), mv[k]);
-                                x = fminf(fmaxf(x, p.lo), p.hi);
-                                b[k] = (uint32_t)__float_as_int(__fadd_rn(x, magic)) + p.zp1;
-                            }
-                            w[g4] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040),
-                                                0x5410) + p.zp4;
-                        }
-                        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-                        continue;
-                    }
                     uint32_t q[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -403,7 +477,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
             if (quarter == 0 && lane == 0) cv_stamp(p, 4, i);
-            aph ^= 1;
         }
     }
 
@@ -413,6 +486,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem_base);
+    }
+    if (threadIdx.x == 0 && p.trace && blockIdx.x < 160) {  // per-CTA exit stamp
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8704 + 160 + blockIdx.x] = t;
     }
 }
 
@@ -429,8 +507,9 @@ CvParams make_params(const ConvArgs& a) {
     p.nq = p.oc_pad + 16;
     p.rblocks = (a.h + ROWS - 1) / ROWS;
     p.units = a.nb * p.rblocks;
-    p.plane_bytes = align_up((ROWS + 2) * p.wp * 16, 128);
-    p.halo_bytes = p.planes * p.plane_bytes;
+    p.nacc = p.nq <= 128 ? MAX_ACC : 2;  // 512 TMEM columns
+    p.acc_cols = 512 / p.nacc;
+    p.halo_bytes = (ROWS + 2) * p.wp * p.c;
     p.pb = a.pw->data;
     p.np = a.pw->np;
     p.img = a.pw->conv_img;
@@ -441,13 +520,14 @@ CvParams make_params(const ConvArgs& a) {
     p.relu = a.raw ? 0 : a.ep->relu;
     p.rounding = a.raw ? 0 : a.ep->rounding;
     p.fast = (!a.raw && p.zp_c >= 0 && p.zp_c <= 255) ? 1 : 0;
-    p.debug_noepi = getenv("Q8G_CONV_NOEPI") != nullptr;
-    p.lo = p.relu ? 0.0f : (float)(-p.zp_c);
-    p.hi = (float)(255 - p.zp_c);
-    p.zp1 = p.relu ? 0u : (uint32_t)p.zp_c;
-    p.zp4 = p.relu ? (uint32_t)p.zp_c * 0x01010101u : 0u;
+    p.debug = getenv("Q8G_CONV_DEBUG") ? std::atoi(getenv("Q8G_CONV_DEBUG")) : 0;
     p.y = a.y;
     p.trace = tc_trace_buffer_ptr();
+    // as many halo buffers as fit next to the operand image (>= 2)
+    int maxbuf = MAX_BUF;
+    if (const char* e = getenv("Q8G_CONV_NBUF")) maxbuf = std::max(2, std::min(MAX_BUF, std::atoi(e)));
+    for (p.nbuf = maxbuf; p.nbuf > 2 && cv_layout(p).total > 232448; --p.nbuf) {
+    }
     return p;
 }
 
@@ -468,10 +548,12 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     CUtensorMap tmap;
     cuuint64_t dims[4] = {(cuuint64_t)a.c, (cuuint64_t)a.w, (cuuint64_t)a.h, (cuuint64_t)a.nb};
     cuuint64_t strides[3] = {(cuuint64_t)a.c, (cuuint64_t)a.w * a.c, (cuuint64_t)a.h * a.w * a.c};
-    cuuint32_t box[4] = {16, (cuuint32_t)(a.w + 2), (cuuint32_t)(ROWS + 2), 1};
+    cuuint32_t box[4] = {(cuuint32_t)a.c, (cuuint32_t)(a.w + 2), (cuuint32_t)(ROWS + 2), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(a.x), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            a.c == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : a.c == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     const CvLayout L = cv_layout(p);
@@ -503,7 +585,7 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     const int threads = 128 + 32 * EPI_WARPS;
     auto go = [&](auto kern) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-        if (e == cudaSuccess) kern<<<grid, threads, L.total, s>>>(tmap, p);
+        if (e == cudaSuccess) e = launch_with_pdl(kern, dim3(grid), dim3(threads), L.total, s, tmap, p);
         return e;
     };
     cudaError_t e;

@@ -126,6 +126,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * NBUF + 2 + a); };
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmemptr_off);
+    ptx::griddep_launch_dependents();
+
+    // global-memory-free prologue first (overlaps the previous grid under PDL)
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_x);
+        for (int b = 0; b < NBUF; ++b) {
+            ptx::mbar_init(full_bar(b), 1);
+            ptx::mbar_init(empty_bar(b), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull_bar(a), 1);
+            ptx::mbar_init(tempty_bar(a), EPI_WARPS);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+    ptx::griddep_wait();
 
     // ---- block-diagonal B = [W | Z] for every channel group (built once):
     // rows 0-15 W[t][c'] on the diagonal, rows 16-31 -zp_w[c'] on the diagonal
@@ -152,19 +169,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
-    if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmap_x);
-        for (int b = 0; b < NBUF; ++b) {
-            ptx::mbar_init(full_bar(b), 1);
-            ptx::mbar_init(empty_bar(b), 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(tfull_bar(a), 1);
-            ptx::mbar_init(tempty_bar(a), EPI_WARPS);
-        }
-        ptx::fence_mbar_init();
-    }
-    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -410,9 +414,9 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
     }
     int grid = sm_count(dev);
     if (grid > p.units) grid = p.units;
-    dwconv_tc_kernel<<<grid, 128 + 32 * EPI_WARPS, L.total, s>>>(tmap, p);
+    const cudaError_t e = launch_with_pdl(dwconv_tc_kernel, dim3(grid), dim3(128 + 32 * EPI_WARPS), L.total, s, tmap, p);
     count_launch(kFamDwTc);
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace q8g

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) sk_stamp(p, 0);
     const uint32_t rank = ptx::cluster_ctarank();
     const int tile = blockIdx.x / S;
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     cluster_arrive_release();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
+    ptx::griddep_wait();  // PDL: the prologue above overlapped the previous grid
     if (threadIdx.x == 0) sk_stamp(p, 1);
 
     if (warp == 0) {
@@ -430,13 +432,15 @@ cudaError_t launch_sk(const GemmArgs& g, cudaStream_t s) {
     cfg.blockDim = dim3(RS ? 384 : 256);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = S;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, p);
     count_launch(kFamGemmTcSmallM);
     return e;

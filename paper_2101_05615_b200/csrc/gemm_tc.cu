@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) trace_stamp(p, 0);
     const uint32_t rank = CN > 1 ? ptx::cluster_ctarank() : 0;
     const uint32_t sA = base + Cfg::A_OFF, sB = base + Cfg::B_OFF;
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     if (CN > 1) ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
+    ptx::griddep_wait();  // PDL: the prologue above overlapped the previous grid
     if (threadIdx.x == 0) trace_stamp(p, 1);
 
     const int num_clusters = gridDim.x / CN;
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
 // debug phase trace (env Q8G_TC_TRACE=1): 8 globaltimer stamps per CTA of the
 // most recent launch, read back with q8g_debug_tc_trace()
 constexpr int kTraceCtas = 1024;
-constexpr int kTraceWords = 8 * kTraceCtas + 512;  // + per-k-block / per-unit stamps of CTA 0
+constexpr int kTraceWords = 8 * kTraceCtas + 2048;  // + per-k-block / per-unit stamps of CTA 0, per-CTA conv spans
 unsigned long long* tc_trace_buffer() {
     static unsigned long long* buf = nullptr;
     static bool enabled = getenv("Q8G_TC_TRACE") != nullptr;
@@ -498,13 +500,22 @@ cudaError_t launch_variant(const GemmArgs& g, cudaStream_t s) {
     cfg.blockDim = dim3(RS ? 384 : 256);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CN;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (CN > 1) {  // cluster launch only when A is multicast
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CN;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = CN > 1 ? 1 : 0;  // plain launch unless A is multicast
+    cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, p);
     count_launch((CN > 1 || BN < 256) ? kFamGemmTcSmallM : kFamGemmTcLargeM);
     return e;

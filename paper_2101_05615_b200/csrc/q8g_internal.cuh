@@ -199,5 +199,24 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
                                 uint8_t* y, cudaStream_t s);
 
 int sm_count(int device);
+// programmatic dependent launch for the tensor-core kernels (env Q8G_PDL=0
+// disables): the kernels trigger their dependents at entry and run their
+// global-memory-free prologue before griddepcontrol.wait
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_with_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 }  // namespace q8g

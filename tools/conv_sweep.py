@@ -38,6 +38,37 @@ def time_graph(launches, reps=5):
     return float(np.median(ts))
 
 
+def time_graph_batched(launches, reps=5, rounds=8):
+    """One event pair around rounds x len(launches) back-to-back launches in
+    one graph: per-launch time including the inter-kernel gap but without
+    per-launch event records."""
+    stream = torch.cuda.current_stream()
+    for f in launches:
+        f()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(rounds):
+            for f in launches:
+                f()
+    ts = []
+    for _ in range(reps):
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3 / (rounds * len(launches)))
+    return float(np.median(ts))
+
+
+BATCHED = False
+
+
+def timed(launches):
+    return time_graph_batched(launches) if BATCHED else time_graph(launches)
+
+
 def c3(nsets=4):
     nb, h, w, c, oc = 32, 56, 56, 64, 64
     rng = np.random.default_rng(0)
@@ -50,7 +81,7 @@ def c3(nsets=4):
     pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
     xs = [torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device="cuda") for _ in range(nsets)]
     ys = [torch.empty((nb, h, w, oc), dtype=torch.uint8, device="cuda") for _ in range(nsets)]
-    us = time_graph([lambda i=i: q8.execute_conv3x3(xs[i], pw, ys[i], pipe) for i in range(nsets)])
+    us = timed([lambda i=i: q8.execute_conv3x3(xs[i], pw, ys[i], pipe) for i in range(nsets)])
     ops = 2.0 * nb * h * w * oc * 9 * c
     byts = 2 * nb * h * w * c + 9 * c * oc + 16 * oc
     print(f"C3 conv3x3 32x56x56x64->64: {us:9.2f} us  {ops / us / 1e6:8.1f} TOPS  {byts / us / 1e3:8.1f} GB/s "
@@ -68,7 +99,7 @@ def c4(nsets=3):
     f = q8.DepthwiseFilter(wt, rp, relu=True)
     xs = [torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device="cuda") for _ in range(nsets)]
     ys = [torch.empty((nb, h, w, c), dtype=torch.uint8, device="cuda") for _ in range(nsets)]
-    us = time_graph([lambda i=i: q8.execute_dwconv3x3(xs[i], f, ys[i]) for i in range(nsets)])
+    us = timed([lambda i=i: q8.execute_dwconv3x3(xs[i], f, ys[i]) for i in range(nsets)])
     ops = 2.0 * 9 * nb * h * w * c
     byts = 2 * nb * h * w * c + 9 * c + 16 * c
     print(f"C4 dwconv3x3 32x112x112x256: {us:9.2f} us  {ops / us / 1e6:8.1f} TOPS  {byts / us / 1e3:8.1f} GB/s "
@@ -79,7 +110,9 @@ if __name__ == "__main__":
     torch.cuda.set_stream(torch.cuda.Stream())
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="both")
+    ap.add_argument("--batched", action="store_true", help="one event pair around many back-to-back launches")
     a = ap.parse_args()
+    BATCHED = a.batched
     if a.which in ("c3", "both"):
         c3()
     if a.which in ("c4", "both"):

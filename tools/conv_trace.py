@@ -29,18 +29,24 @@ def main():
     for _ in range(3):
         q8.execute_conv3x3(x, pw, y, pipe)
     torch.cuda.synchronize()
-    buf = (C.c_uint64 * (8 * 1024 + 512))()
+    buf = (C.c_uint64 * (8 * 1024 + 2048))()
     _lib.load().q8g_debug_tc_trace(buf, 2048)
     a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
     units = a[8192:8192 + 320].reshape(5, 64)
-    t0 = min(units[0][units[0] > 0].min(), a[8192 + 320])
-    print(f"prologue done at {(a[8192 + 320] - t0) / 1e3:.2f} us (relative to first stamp)")
+    t0 = a[8192 + 321]
+    ent, ext = a[8704:8704 + 148], a[8704 + 160:8704 + 160 + 148]
+    print(f"grid span: first entry {(ent.min() - t0) / 1e3:.2f}  last entry {(ent.max() - t0) / 1e3:.2f}  "
+          f"first exit {(ext.min() - t0) / 1e3:.2f}  last exit {(ext.max() - t0) / 1e3:.2f} us; "
+          f"CTA0 exit {(ext[0] - t0) / 1e3:.2f}")
+    print(f"kernel entry at 0; barriers+image issued {(a[9344] - t0) / 1e3:.2f}, guards zeroed {(a[9345] - t0) / 1e3:.2f}, "
+          f"TMEM allocated {(a[9346] - t0) / 1e3:.2f}, prologue done at {(a[8192 + 320] - t0) / 1e3:.2f} us")
     n = int((units[0] > 0).sum())
     tl = a[8192 + 384:8192 + 448]
-    print("unit  halo_issued  mma_start  mma_commit  epi_start  epi_done  tmem_landed (us)")
+    w5, w6 = a[9216:9216 + 64], a[9280:9280 + 64]
+    print("unit  halo_issued  mma_start  mma_commit  epi_start  epi_done  tmem_landed  past_tempty  past_full (us)")
     for i in range(n):
         print(f"{i:4d} " + " ".join(f"{(units[j, i] - t0) / 1e3:9.2f}" for j in range(5)) +
-              f" {(tl[i] - t0) / 1e3:9.2f}")
+              f" {(tl[i] - t0) / 1e3:9.2f} {(w5[i] - t0) / 1e3:9.2f} {(w6[i] - t0) / 1e3:9.2f}")
 
 
 if __name__ == "__main__":

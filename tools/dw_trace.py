@@ -28,7 +28,7 @@ def main():
     for _ in range(3):
         q8.execute_dwconv3x3(x, f, y)
     torch.cuda.synchronize()
-    buf = (C.c_uint64 * (8 * 1024 + 512))()
+    buf = (C.c_uint64 * (8 * 1024 + 2048))()
     _lib.load().q8g_debug_tc_trace(buf, 2048)
     a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)[8192:8192 + 320].reshape(5, 64)
     n = int((a[0] > 0).sum())

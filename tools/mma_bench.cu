@@ -49,7 +49,21 @@ __global__ void bench(int layout, int iters, unsigned long long* out) {
         unsigned long long t0 = 0, t1 = 0;
         if (ptx::elect_one()) {
             asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
-            if (layout == 5) {
+            if (layout == 6) {
+                // conv3x3_tc swizzled pattern: A = SW64 rows of 64 B shifted by tap, 2 K-steps
+                const int wp = 58;
+                for (int i = 0; i < iters / 18; ++i)
+                    for (int t = 0; t < 9; ++t) {
+                        const int sh = (t / 3) * wp + (t % 3);
+                        for (int j = 0; j < 2; ++j) {
+                            const uint32_t aa = a + (uint32_t)(sh * 64 + j * 32);
+                            const uint64_t ad6 = (uint64_t)((aa & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
+                                                 ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+                            ptx::mma_i8(tmem, ad6, desc_noswz(b + (uint32_t)(((t * 2 + j) * 2) * N * 16) % 16384, N * 16, 128),
+                                        idesc, (t | j) != 0);
+                        }
+                    }
+            } else if (layout == 5) {
                 // conv3x3_tc pattern: 9 taps x 2 K-steps, A = tap-shifted window of
                 // plane pair (LBO = plane stride 3712 B), B steps 2*N*16 per (tap, j)
                 const int wp = 58, plane = 3712;
@@ -104,11 +118,16 @@ void run(int layout, const char* name) {
 int main(int argc, char** argv) {
     if (argc > 1) g_grid = atoi(argv[1]);
     std::printf("grid = %d CTAs\n", g_grid);
-    const char* names[6] = {"SW128 K-major", "no-swizzle (LBO 2KB)", "no-swizzle (LBO 16B)",
-                            "noswz A+16B/MMA, 4 D tiles", "noswz A+4KB/MMA, 4 D tiles", "conv3x3 pattern"};
+    const char* names[7] = {"SW128 K-major", "no-swizzle (LBO 2KB)", "no-swizzle (LBO 16B)",
+                            "noswz A+16B/MMA, 4 D tiles", "noswz A+4KB/MMA, 4 D tiles", "conv3x3 pattern",
+                            "conv3x3 SW64 pattern"};
     if (argc > 2) {
         run<80>(5, names[5]);
         run<32>(5, names[5]);
+        run<80>(6, names[6]);
+        run<32>(6, names[6]);
+        run<144>(6, names[6]);
+        run<80>(0, names[0]);
         return 0;
     }
     for (int l = 0; l < 5; ++l) {

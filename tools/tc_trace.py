@@ -43,7 +43,7 @@ def main():
     torch.cuda.synchronize()
     q8.execute_gemm(a, pw, c, pipe)
     torch.cuda.synchronize()
-    buf = (C.c_uint64 * (8 * 1024 + 256))()
+    buf = (C.c_uint64 * (8 * 1024 + 2048))()
     nct = _lib.load().q8g_debug_tc_trace(buf, 2048)
     allw = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
     t = allw[:8 * 1024].reshape(1024, 8)[:nct]
