@@ -364,6 +364,9 @@ int q8g_epilogue_create(const q8g_packed_b* pb, const q8g_requant_params* p,
     ep->rounding = p->rounding;
     ep->relu = p->relu ? 1 : 0;
     ep->need_rowsum = need_rowsum;
+    ep->fast_f32 = p->rounding == Q8G_ROUND_F32_RNE && p->zp_c >= 0 && p->zp_c <= 255;
+    for (int j = 0; j < pb->n && ep->fast_f32; ++j)
+        if (!(rec[j].mf < 7.9228163e28f)) ep->fast_f32 = false;  // 2^96; also rejects inf
     cudaError_t e;
     if ((e = cudaMalloc(&ep->rec, sizeof(EpiRecord) * pb->np)) != cudaSuccess ||
         (e = cudaMemcpy(ep->rec, rec.data(), sizeof(EpiRecord) * pb->np, cudaMemcpyHostToDevice)) !=

@@ -519,7 +519,7 @@ CvParams make_params(const ConvArgs& a) {
     p.zp_c = a.raw ? 0 : a.ep->zp_c;
     p.relu = a.raw ? 0 : a.ep->relu;
     p.rounding = a.raw ? 0 : a.ep->rounding;
-    p.fast = (!a.raw && p.zp_c >= 0 && p.zp_c <= 255) ? 1 : 0;
+    p.fast = (!a.raw && a.ep->fast_f32) ? 1 : 0;
     p.debug = getenv("Q8G_CONV_DEBUG") ? std::atoi(getenv("Q8G_CONV_DEBUG")) : 0;
     p.y = a.y;
     p.trace = tc_trace_buffer_ptr();

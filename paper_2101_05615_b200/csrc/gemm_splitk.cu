@@ -10,18 +10,25 @@
 // of every stage is weights and the mainloop runs at HBM speed.
 //
 // Exchange: rank r owns output columns [r*OWN, (r+1)*OWN) of the cluster's
-// BN-wide tile.  After its mainloop each rank stages the partial columns the
-// other ranks own (plus its partial row sums) in its now-idle pipeline smem
-// and pushes them with one cp.async.bulk smem->peer-smem copy per peer; the
-// copy completes on the owner's mbarrier.  (Register-issued
-// st.shared::cluster stores were measured at ~25 GB/s per SM: 1.9 us for the
-// 48 KB exchange.)
+// BN-wide tile.  After its mainloop each rank writes the partial columns the
+// other ranks own (plus its partial row sums) from TMEM to an L2-resident
+// workspace, the cluster passes one release/acquire barrier, and each owner
+// reads its S-1 slots back from L2 (all loads in flight at once).  Eight
+// warps share the exchange and the epilogue (the producer / MMA / idle warps
+// join once the mainloop is done).  An SM-to-SM (DSMEM) exchange measured
+// ~25 GB/s per SM: 1.9-2 us for the 48 KB per CTA, register stores and bulk
+// smem->peer-smem copies alike, plus a wait for the outgoing copies.
 //
 // Same drop-in semantics as gemm_tc.cu (engine.hpp:59-169 + Requantize,
 // pipeline.hpp:157-210); int32 addition is associative so the split is
 // bit-exact.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
 
 #include "ptx.cuh"
 #include "q8g_internal.cuh"
@@ -47,14 +54,12 @@ struct SkCfg {
     static constexpr int SLOT_BYTES = SLOT_PART + BM * 4;
     static constexpr int A_OFF = 0;  // also the send staging area after the mainloop
     static constexpr int B_OFF = STAGES * A_STAGE;
-    static constexpr int RECV_OFF = B_OFF + STAGES * B_STAGE;  // [S-1] slots
-    static constexpr int OWNRS_OFF = RECV_OFF + (S - 1) * SLOT_BYTES;
+    static constexpr int OWNRS_OFF = B_OFF + STAGES * B_STAGE;
     static constexpr int REC_OFF = OWNRS_OFF + BM * 4;  // [OWN] EpiRecord
     static constexpr int BAR_OFF = REC_OFF + OWN * 16;
-    static constexpr int NUM_BARS = 3 * STAGES + 3;  // full, empty, rsdone, tfull, recvfull, rsready
+    static constexpr int NUM_BARS = 3 * STAGES + 2;  // full, empty, rsdone, tfull, rsready
     static constexpr int TMEMPTR_OFF = BAR_OFF + NUM_BARS * 8;
     static constexpr int SMEM_BYTES = TMEMPTR_OFF + 16 + 1024;
-    static_assert((S - 1) * SLOT_BYTES <= STAGES * A_STAGE, "send staging must fit the A stages");
     static_assert(SLOT_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
     static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
@@ -66,14 +71,18 @@ struct SkParams {
     const EpiRecord* rec;
     int32_t zp_c;
     int relu;
+    int fast;  // F32_RNE fast requant allowed (q8g_epilogue::fast_f32)
     const int32_t* bias_add;
     void* c;
     int ldc;
+    // L2 exchange workspace [tile][owner][S-1 slots] of SLOT_BYTES; null =
+    // push the slots into the owners' smem (DSMEM)
+    uint8_t* ws;
     unsigned long long* trace;  // debug stamps (Q8G_TC_TRACE), else null
 };
 
-// same slots as gemm_tc.cu: 0 entry, 1 prologue, 2 first TMA, 3 first stage,
-// 4 last MMA commit, 5 epilogue start, 6 exchange landed, 7 stores issued;
+// slots: 0 entry, 1 prologue, 2 first TMA, 3 first stage, 4 last MMA commit,
+// 5 past the exchange's cluster barrier, 6 exchange stores issued, 7 done;
 // per-k-block stamps of CTA 0
 __device__ __forceinline__ void sk_stamp(const SkParams& p, int slot) {
     if (p.trace) {
@@ -90,24 +99,35 @@ __device__ __forceinline__ void sk_kb(const SkParams& p, int which, int i) {
     }
 }
 
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
 __device__ __forceinline__ void cluster_arrive_release() {
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait_acquire() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// smem -> peer smem bulk copy, completing tx bytes on the peer's mbarrier
-__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
-                                               uint32_t mbar_cluster) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_cluster),
-        "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
-        : "memory");
+// L2-only 16-byte global store / load (split-K exchange workspace)
+__device__ __forceinline__ void st_cg_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.cg.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_cg_s32(const void* p) {
+    int32_t v;
+    asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_cg_s32(void* p, int32_t v) {
+    asm volatile("st.global.cg.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// d = {c[15:0], sat_u8(a), sat_u8(b)} (one I2IP)
+__device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
 }
 
 template <int BN, int S, int STAGES, int MODE, bool RS>
@@ -115,7 +135,8 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmap_a, const SkParams p) {
     using Cfg = SkCfg<BN, S, STAGES>;
     constexpr int OWN = Cfg::OWN;
-    static_assert(OWN % 16 == 0, "owned column block must be a multiple of 16");
+    constexpr int NH = OWN / 16;  // 16-column chunks per owned block, split over 2 epilogue groups
+    static_assert(OWN % 32 == 0, "owned column block must be a multiple of 32");
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     const uint32_t base = (raw_addr + 1023u) & ~1023u;
@@ -139,8 +160,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto rsdone_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
     const uint32_t tfull = bar0 + 8u * (3 * STAGES);
-    const uint32_t recvfull = bar0 + 8u * (3 * STAGES + 1);
-    const uint32_t rsready = bar0 + 8u * (3 * STAGES + 2);
+    const uint32_t rsready = bar0 + 8u * (3 * STAGES + 1);
     int32_t* ownrs = reinterpret_cast<int32_t*>(smem + Cfg::OWNRS_OFF);
     const int4* recs = reinterpret_cast<const int4*>(smem + Cfg::REC_OFF);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + Cfg::TMEMPTR_OFF);
@@ -153,18 +173,12 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             ptx::mbar_init(rsdone_bar(s), 4);
         }
         ptx::mbar_init(tfull, 1);
-        ptx::mbar_init(recvfull, 1);
         ptx::mbar_init(rsready, 4);
         ptx::fence_mbar_init();
-        // all S-1 peer slots will complete on recvfull
-        ptx::mbar_arrive_expect_tx(recvfull, (S - 1) * Cfg::SLOT_BYTES);
     }
     if (warp == 2) ptx::tmem_alloc<Cfg::TMEM_COLS>(ptx::smem_u32(tmem_ptr));
     ptx::tc_fence_before();
     __syncthreads();
-    // early arrive: "my barriers are initialised, expect_tx is armed"; the
-    // matching wait sits right before the first remote copy
-    cluster_arrive_release();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
     ptx::griddep_wait();  // PDL: the prologue above overlapped the previous grid
@@ -247,88 +261,85 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         ownrs[r] = (int32_t)sum;  // partial over this rank's K-slice
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(rsready);
-    } else if (warp >= 4 && warp < 8) {
-        const int ew = warp - 4;
-        const int r = ew * 32 + lane;
+    }
+    if (warp < 8) {
+        // ------------------------------------------------ exchange + epilogue
+        // two groups of 4 warps: warps 4-7 (g 0) and, once their roles are
+        // done, warps 0-3 (g 1); a warp reads TMEM lanes 32*(warp%4).., each
+        // group takes every other 16-column chunk of a block
+        const int g = warp < 4 ? 1 : 0;
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;  // tile row
+        const uint32_t lane_base = tmem_base + ((uint32_t)(q4 * 32) << 16);
         // stage the owned columns' epilogue records while the mainloop runs
-        if (MODE != 0 && r < OWN) {
+        if (g == 0 && MODE != 0 && r < OWN) {
             const int4 r4 = __ldg(reinterpret_cast<const int4*>(p.rec + n0 + (int)rank * OWN + r));
             reinterpret_cast<int4*>(smem + Cfg::REC_OFF)[r] = r4;
         }
-        ptx::mbar_wait(tfull, 0);  // mainloop done: the A stages are free for staging
+        ptx::mbar_wait(tfull, 0);
         ptx::tc_fence_after();
-        if (warp == 4 && lane == 0) sk_stamp(p, 5);
         int32_t my_rs = 0;
         if (RS) {
             ptx::mbar_wait(rsready, 0);
             my_rs = ownrs[r];
         }
-        // ---- stage the partial columns each peer owns: send slot qi for peer
-        // q = rank + 1 + qi (mod S), layout [quad][row] int4 then [row] row sum
+        // ---- write the partial columns each peer owns (and the partial row
+        // sums) from TMEM to the L2 workspace, coalesced [quad][row] int4
 #pragma unroll 1
         for (int qi = 0; qi < S - 1; ++qi) {
             const int q = ((int)rank + 1 + qi) % S;
-            uint8_t* slot = smem + Cfg::A_OFF + qi * Cfg::SLOT_BYTES;
+            const int dslot = ((int)rank - q + S) % S - 1;  // at owner q: slot of this source
+            uint8_t* slot = p.ws + ((size_t)(tile * S + q) * (S - 1) + dslot) * Cfg::SLOT_BYTES;
 #pragma unroll
-            for (int h = 0; h < OWN / 16; ++h) {
+            for (int h = g; h < NH; h += 2) {
                 uint32_t v[16];
-                ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(q * OWN + h * 16), v);
+                ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(q * OWN + h * 16), v);
                 ptx::tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 16; j += 4) {
-                    const int c4 = h * 4 + j / 4;
-                    *reinterpret_cast<uint4*>(slot + ((size_t)c4 * BM + r) * 16) =
-                        make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                }
+                for (int j = 0; j < 16; j += 4)
+                    st_cg_v4(slot + ((size_t)(h * 4 + j / 4) * BM + r) * 16, v[j], v[j + 1], v[j + 2], v[j + 3]);
             }
-            reinterpret_cast<int32_t*>(slot + Cfg::SLOT_PART)[r] = my_rs;
+            if (g == 0 && RS) st_cg_s32(slot + Cfg::SLOT_PART + r * 4, my_rs);
         }
-        // generic-proxy smem writes -> visible to the bulk-copy (async) proxy
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 4) {
-            cluster_wait_acquire();  // every peer has armed its recvfull barrier
-            if (lane == 0) {
-#pragma unroll 1
-                for (int qi = 0; qi < S - 1; ++qi) {
-                    const int q = ((int)rank + 1 + qi) % S;
-                    // at owner q, the slot of source rank s is (s - q + S) % S - 1
-                    const int dslot = ((int)rank - q + S) % S - 1;
-                    bulk_s2cluster(mapa(base + Cfg::RECV_OFF + dslot * Cfg::SLOT_BYTES, q),
-                                   base + Cfg::A_OFF + qi * Cfg::SLOT_BYTES, Cfg::SLOT_BYTES, mapa(recvfull, q));
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            __syncwarp();
-        }
-        // ---- reduce the owned columns: own partial + S-1 received partials
-        ptx::mbar_wait(recvfull, 0);
+        // group 0's staged records -> group 1; then one release/acquire
+        // cluster barrier orders every rank's workspace writes before the reads
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (warp == 4 && lane == 0) sk_stamp(p, 6);
+        cluster_arrive_release();
+        cluster_wait_acquire();
+        if (warp == 4 && lane == 0) sk_stamp(p, 5);
+        // ---- reduce the owned columns: own partial + the S-1 received slots,
+        // all loads in flight at once (one L2 round trip)
+        const uint8_t* recv = p.ws + (size_t)(tile * S + (int)rank) * (S - 1) * Cfg::SLOT_BYTES;
         const int row = m0 + r;
         int32_t rowsum = my_rs;
-        const uint8_t* recv = smem + Cfg::RECV_OFF;
         if (RS) {
 #pragma unroll
-            for (int sl = 0; sl < S - 1; ++sl)
-                rowsum += reinterpret_cast<const int32_t*>(recv + sl * Cfg::SLOT_BYTES + Cfg::SLOT_PART)[r];
+            for (int sl = 0; sl < S - 1; ++sl) rowsum += ld_cg_s32(recv + sl * Cfg::SLOT_BYTES + Cfg::SLOT_PART + r * 4);
         }
+        uint4 rx[NH / 2][S - 1][4];
 #pragma unroll
-        for (int h = 0; h < OWN / 16; ++h) {
+        for (int hh = 0; hh < NH / 2; ++hh)
+#pragma unroll
+            for (int sl = 0; sl < S - 1; ++sl)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    rx[hh][sl][j] = ld_cg_v4(recv + sl * Cfg::SLOT_BYTES + ((size_t)((g + 2 * hh) * 4 + j) * BM + r) * 16);
+#pragma unroll
+        for (int hh = 0; hh < NH / 2; ++hh) {
+            const int h = g + 2 * hh;
             uint32_t v[16];
-            ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(rank * OWN + h * 16), v);
+            ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(rank * OWN + h * 16), v);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int sl = 0; sl < S - 1; ++sl) {
+            for (int sl = 0; sl < S - 1; ++sl)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const uint4 x =
-                        *reinterpret_cast<const uint4*>(recv + sl * Cfg::SLOT_BYTES + ((size_t)(h * 4 + j) * BM + r) * 16);
-                    v[4 * j + 0] += x.x;
-                    v[4 * j + 1] += x.y;
-                    v[4 * j + 2] += x.z;
-                    v[4 * j + 3] += x.w;
+                    v[4 * j + 0] += rx[hh][sl][j].x;
+                    v[4 * j + 1] += rx[hh][sl][j].y;
+                    v[4 * j + 2] += rx[hh][sl][j].z;
+                    v[4 * j + 3] += rx[hh][sl][j].w;
                 }
-            }
             const int col0 = n0 + (int)rank * OWN + h * 16;
             if (row >= p.rows || col0 >= p.n) continue;
             if (MODE == 0) {
@@ -351,8 +362,29 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                     for (int j = 0; j < 16; ++j)
                         if (col0 + j < p.n) dst[j] = out[j];
                 }
+                continue;
+            }
+            uint32_t packed[4];
+            if (MODE == 1 && p.fast) {
+                // F32_RNE, 0 <= zp_c <= 255, finite multipliers: magic-add
+                // rounding + saturating pack (exact; see conv_tc.cu epi_f32_fast)
+                const int32_t zoff = 0x4B400000 - p.zp_c;
+                const float floor_x = p.relu ? 0.0f : -8388608.0f;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    int32_t rr[4];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int j = w * 4 + b;
+                        const int4 r4 = recs[h * 16 + j];
+                        const int32_t adj = (int32_t)(v[j] + (uint32_t)r4.x - (uint32_t)r4.y * (uint32_t)rowsum);
+                        float x = __fmul_rn(__int2float_rn(adj), __int_as_float(r4.z));
+                        x = fmaxf(x, floor_x);
+                        rr[b] = __float_as_int(__fadd_rn(x, 12582912.0f)) - zoff;
+                    }
+                    packed[w] = pack_sat_u8(rr[1], rr[0], pack_sat_u8(rr[3], rr[2], 0u));
+                }
             } else {
-                uint32_t packed[4];
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     uint32_t word = 0;
@@ -370,23 +402,22 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                     }
                     packed[w] = word;
                 }
-                uint8_t* dst = reinterpret_cast<uint8_t*>(p.c) + (size_t)row * p.ldc + col0;
-                const bool vec = (col0 + 16 <= p.n) && ((p.ldc & 15) == 0) &&
-                                 ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-                if (vec) {
-                    *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-                } else {
-                    for (int j = 0; j < 16; ++j)
-                        if (col0 + j < p.n) dst[j] = (uint8_t)(packed[j / 4] >> (8 * (j % 4)));
-                }
+            }
+            uint8_t* dst = reinterpret_cast<uint8_t*>(p.c) + (size_t)row * p.ldc + col0;
+            const bool vec = (col0 + 16 <= p.n) && ((p.ldc & 15) == 0) &&
+                             ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+            if (vec) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            } else {
+                for (int j = 0; j < 16; ++j)
+                    if (col0 + j < p.n) dst[j] = (uint8_t)(packed[j / 4] >> (8 * (j % 4)));
             }
         }
-        if (warp == 4) {
-            // the staged source smem must stay valid until the copies have read it
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();
-        }
         if (warp == 4 && lane == 0) sk_stamp(p, 7);
+    } else {
+        // row-sum warps: their arrival in the cluster barrier's one phase
+        __syncwarp();
+        cluster_arrive_release();
     }
 
     __syncwarp();
@@ -396,6 +427,29 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
     }
+}
+
+// split-K exchange workspace, one per (device, stream) so concurrent streams
+// never share it; grow-only and never freed (captured graphs keep the
+// pointer).  Null on allocation failure or when a capture is in progress and
+// no large-enough workspace exists yet (the caller then uses the non-split
+// kernel).
+uint8_t* splitk_workspace(int dev, cudaStream_t s, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, std::pair<uint8_t*, size_t>> ws;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& slot = ws[{dev, s}];
+    if (slot.second >= bytes) return slot.first;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    uint8_t* buf = nullptr;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    slot = {buf, bytes};  // a smaller predecessor stays allocated (may be in a graph)
+    return buf;
 }
 
 template <int BN, int S, int STAGES, int MODE, bool RS>
@@ -422,11 +476,14 @@ cudaError_t launch_sk(const GemmArgs& g, cudaStream_t s) {
     p.rec = g.ep ? g.ep->rec : nullptr;
     p.zp_c = g.ep ? g.ep->zp_c : 0;
     p.relu = g.ep ? g.ep->relu : 0;
+    p.fast = (g.ep && g.ep->fast_f32) ? 1 : 0;
     p.bias_add = g.bias_add;
     p.c = g.c;
     p.ldc = g.ldc;
     p.trace = tc_trace_buffer_ptr();
     const int tiles = ceil_div_i(g.rows, BM) * p.num_n_tiles;
+    p.ws = splitk_workspace(dev, s, (size_t)tiles * S * (S - 1) * Cfg::SLOT_BYTES);
+    if (!p.ws) return cudaErrorNotSupported;  // caller falls back to the non-split kernel
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tiles * S);
     cfg.blockDim = dim3(RS ? 384 : 256);
@@ -460,6 +517,12 @@ cudaError_t launch_sk_modes(const GemmArgs& g, cudaStream_t s) {
 // split-K applies when every rank gets at least one k-block
 bool splitk_supported(const GemmArgs& g) { return g.pb->kp / kKBlock >= 4; }
 
-cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s) { return launch_sk_modes<128, 4, 5>(g, s); }
+cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s) {
+    static const int stages = [] {  // tuning knob: Q8G_SK_STAGES=5
+        const char* e = getenv("Q8G_SK_STAGES");
+        return e ? std::atoi(e) : 6;
+    }();
+    return stages == 5 ? launch_sk_modes<128, 4, 5>(g, s) : launch_sk_modes<128, 4, 6>(g, s);
+}
 
 }  // namespace q8g

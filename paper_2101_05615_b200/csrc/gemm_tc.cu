@@ -582,12 +582,18 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
         case 4: return launch_modes<128, 2, 6>(g, s);
         case 5: return launch_modes<256, 1, 4>(g, s);
         case 6:
-            if (splitk_supported(g)) return launch_gemm_splitk(g, s);
+            if (splitk_supported(g)) {
+                const cudaError_t e = launch_gemm_splitk(g, s);
+                if (e != cudaErrorNotSupported) return e;  // else: no workspace -> non-split kernel
+            }
             break;
         default: break;
     }
     if (tile_kind == kSmallM) {
-        if (splitk_supported(g)) return launch_gemm_splitk(g, s);
+        if (splitk_supported(g)) {
+            const cudaError_t e = launch_gemm_splitk(g, s);
+            if (e != cudaErrorNotSupported) return e;  // else: no workspace -> non-split kernel
+        }
         return launch_modes<32, 1, 10>(g, s);
     }
     return launch_modes<256, 1, 4>(g, s);

@@ -107,6 +107,9 @@ struct q8g_epilogue {
     int rounding = Q8G_ROUND_REF;
     int relu = 0;
     bool need_rowsum = false;  // any zp_b[j] != 0 (pipeline.hpp:114-119)
+    // F32_RNE with 0 <= zp_c <= 255 and every multiplier finite, < 2^96: the
+    // kernels may use the magic-add / saturating-pack requant (exact then)
+    bool fast_f32 = false;
     q8g::EpiRecord* rec = nullptr;  // device, np records
 };
 
