@@ -17,10 +17,11 @@ value     : whole-job int8 TOPS (2*M*N*K per step over all ranks / max-over-
 e2e       : the same metric through the C-ABI host-buffer entry point
             (q8g_gemm_u8s8_requant_host): per step H2D of A from pinned
             memory, the kernel, D2H of the u8 output.
-roofline  : the GEMM kernel's algorithmic bytes / its event-timed average
-            launch duration vs the measured HBM copy bandwidth
-            (MEASURED_PEAKS.json); traffic = ncu dram bytes of the same
-            kernel (profiles/), or null.
+roofline  : the GEMM kernel's algorithmic bytes / its average launch
+            duration over the timed region (K back-to-back launches between
+            one event pair; kernel_ms_isolated = per-launch event pairs) vs
+            the measured HBM copy bandwidth (MEASURED_PEAKS.json); traffic =
+            ncu dram bytes of the same kernel (profiles/), or null.
 cpu_baseline / --impl reference : the reference's own CPU path
             (oracle/_ref: unmodified q8gemm execute_gemm, caller-owned
             std::threads = all host cores) + the restated per-channel fp32
@@ -59,6 +60,23 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
     return 6650.0, 1590.0, "fallback"
+
+
+def max_over_ranks(vals, device, world):
+    """Element-wise max of per-rank timings (the slowest rank sets the step)."""
+    if world <= 1:
+        return [float(v) for v in vals]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
+
+
+def whole_job_tops(m_per_rank, n, k, world, ms_per_step):
+    """Weak scaling: every rank runs an M=m_per_rank stripe; value = all
+    ranks' int8 ops per step / the max-over-ranks step time."""
+    return 2.0 * m_per_rank * n * k * world / (ms_per_step * 1e-3) / 1e12
 
 
 def algorithmic_bytes(m, n, k):
@@ -303,27 +321,30 @@ def run_ours(args):
         e2e_call(i)
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
+    # device-side span on the call's stream: H2D of A, the GEMM, D2H of C and
+    # any host gaps between the (synchronous) calls all fall inside it
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
     for i in range(e2e_steps):
         e2e_call(i)
+    e1.record(stream)
     torch.cuda.synchronize(dev)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s = e0.elapsed_time(e1) * 1e-3 / e2e_steps
     if world > 1:
         dist.barrier()
 
-    # max over ranks
-    vals = torch.tensor([ms, kern_ms, e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, kern_ms, e2e_s = (float(v) for v in vals.cpu())
+    ms, kern_ms, e2e_s = max_over_ranks([ms, kern_ms, e2e_s], dev, world)
 
     if rank == 0:
-        ops_step = 2.0 * m * n * k * world
         ms_step = ms / args.steps
-        value = ops_step / (ms_step * 1e-3) / 1e12
+        value = whole_job_tops(m, n, k, world, ms_step)
         hbm, _, src = peaks()
         abytes = algorithmic_bytes(m, n, k)
-        achieved = abytes / (kern_ms * 1e-3) / 1e9
+        # the dominant (only) kernel's average launch duration over the timed
+        # region: K back-to-back launches between one event pair
+        kern_avg_ms = ms_step / max(1.0, launches_per_step)
+        achieved = abytes / (kern_avg_ms * 1e-3) / 1e9
         traffic = None
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
@@ -338,8 +359,9 @@ def run_ours(args):
                        "graph": "K steps captured in one CUDA graph", "packing": "excluded (prepacked once)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_source": src + " (MEASURED_PEAKS.json hbm_gbs)",
-                         "algorithmic_bytes_per_launch": abytes, "kernel_ms": kern_ms,
-                         "int8_tops_per_launch": 2.0 * m * n * k / (kern_ms * 1e-3) / 1e12},
+                         "algorithmic_bytes_per_launch": abytes, "kernel_ms": kern_avg_ms,
+                         "kernel_ms_isolated": kern_ms,
+                         "int8_tops_per_launch": 2.0 * m * n * k / (kern_avg_ms * 1e-3) / 1e12},
             "e2e": {"value": 2.0 * m * n * k * world / e2e_s / 1e12, "unit": "TOPS",
                     "h2d_bytes_per_step": m * k * world, "d2h_bytes_per_step": m * n * world,
                     "ms_per_step": e2e_s * 1e3, "path": "q8g_gemm_u8s8_requant_host (pinned host buffers)"},

@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     execute_gemm,
     i16_accumulation_exact,
     partition_stripes,
+    stripe_rows,
     prepack_conv3x3_weights,
     prepack_weights,
     select_blocking,

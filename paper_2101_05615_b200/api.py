@@ -84,6 +84,15 @@ def partition_stripes(num_blocks: int, thread_id: int, num_threads: int) -> tupl
 
 # ---------------------------------------------------------------- helpers
 
+def stripe_rows(m: int, thread_id: int, num_threads: int) -> tuple[int, int]:
+    """Rows [r0, r1) of worker `thread_id` of `num_threads`: the balanced,
+    disjoint stripe of 128-row blocks of engine.hpp:40-47.  The same split
+    shards a batch across ranks (one process per GPU, no collective)."""
+    nblk = (m + TILE_M - 1) // TILE_M
+    b0, b1 = partition_stripes(nblk, thread_id, num_threads)
+    return min(b0 * TILE_M, m), min(b1 * TILE_M, m)
+
+
 def _is_dev(x) -> bool:
     return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
 
@@ -406,9 +415,7 @@ def execute_gemm(a, pw: PackedWeight, out, pipeline: OutputPipeline,
             "exceeds 32767; split outliers with a threshold satisfying 255 * (T - 1) * kcb <= 32767 "
             "(see max_i16_split_threshold)")
     pipeline._unsupported()
-    nblk = (m + TILE_M - 1) // TILE_M
-    b0, b1 = partition_stripes(nblk, thread_id, num_threads)
-    r0, r1 = min(b0 * TILE_M, m), min(b1 * TILE_M, m)
+    r0, r1 = stripe_rows(m, thread_id, num_threads)
     if r0 >= r1:
         return
     lib = load()
