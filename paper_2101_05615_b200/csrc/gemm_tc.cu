@@ -33,6 +33,7 @@
 
 #include "ptx.cuh"
 #include "q8g_internal.cuh"
+#include "epilogue.cuh"
 #include "requant.cuh"
 
 namespace q8g {
@@ -64,6 +65,7 @@ struct TcParams {
     const EpiRecord* rec;
     int32_t zp_c;
     int relu;
+    int fast;                 // q8g_epilogue::fast_f32
     const int32_t* bias_add;  // raw writer only
     void* c;
     int ldc;
@@ -88,68 +90,6 @@ __device__ __forceinline__ void trace_kb(const TcParams& p, int which, int kb) {
 }
 
 constexpr int EPI_COLS = 16;  // columns per tcgen05.ld in the epilogue
-
-template <int MODE>
-__device__ __forceinline__ void store_chunk(const TcParams& p, int row, int col0,
-                                            const uint32_t (&v)[EPI_COLS], int32_t rowsum) {
-    // MODE 0: raw int32 (+BiasAdd); 1: requant F32_RNE; 2: requant REF
-    if (MODE == 0) {
-        int32_t* dst = reinterpret_cast<int32_t*>(p.c) + (size_t)row * p.ldc + col0;
-        int32_t out[EPI_COLS];
-#pragma unroll
-        for (int j = 0; j < EPI_COLS; ++j) {
-            int32_t x = (int32_t)v[j];
-            if (p.bias_add && col0 + j < p.n)
-                x = (int32_t)((uint32_t)x + (uint32_t)__ldg(p.bias_add + col0 + j));
-            out[j] = x;
-        }
-        const bool vec = (col0 + EPI_COLS <= p.n) && ((p.ldc & 3) == 0) &&
-                         ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-        if (vec) {
-#pragma unroll
-            for (int j = 0; j < EPI_COLS; j += 4)
-                *reinterpret_cast<int4*>(dst + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < EPI_COLS; ++j)
-                if (col0 + j < p.n) dst[j] = out[j];
-        }
-    } else {
-        uint32_t packed[EPI_COLS / 4];
-#pragma unroll
-        for (int w = 0; w < EPI_COLS / 4; ++w) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int j = w * 4 + b;
-                const int4 r4 = __ldg(reinterpret_cast<const int4*>(p.rec + col0 + j));
-                EpiRecord rc;
-                rc.c = r4.x;
-                rc.zpb = r4.y;
-                uint32_t q;
-                const int32_t adj = adjust((int32_t)v[j], rowsum, rc);
-                if (MODE == 1) {
-                    q = requant_f32(adj, __int_as_float(r4.z), p.zp_c, p.relu);
-                } else {
-                    const double md = __hiloint2double(r4.w, r4.z);
-                    q = requant_ref(adj, md, p.zp_c, p.relu);
-                }
-                word |= q << (8 * b);
-            }
-            packed[w] = word;
-        }
-        uint8_t* dst = reinterpret_cast<uint8_t*>(p.c) + (size_t)row * p.ldc + col0;
-        const bool vec = (col0 + EPI_COLS <= p.n) && ((p.ldc & 15) == 0) &&
-                         ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-        if (vec) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < EPI_COLS; ++j)
-                if (col0 + j < p.n) dst[j] = (uint8_t)(packed[j / 4] >> (8 * (j % 4)));
-        }
-    }
-}
 
 template <int BN, int CN, int STAGES, int MODE, bool RS>
 __global__ void __launch_bounds__(RS ? 384 : 256, 1)
@@ -315,6 +255,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             }
             const int row = m0 + r;
             const bool valid = row < p.rows;
+            const EpiArgs ea{p.rec, p.zp_c, p.relu, p.fast, p.bias_add, p.c, p.ldc, p.n};
 #pragma unroll 1
             for (int ch = 0; ch < BN / EPI_COLS; ++ch) {
                 uint32_t v[EPI_COLS];
@@ -323,7 +264,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 ptx::tmem_ld_32x32b_x16(taddr, v);
                 ptx::tmem_ld_wait();
                 const int col0 = n0 + ch * EPI_COLS;
-                if (valid && col0 < p.n) store_chunk<MODE>(p, row, col0, v, rowsum);
+                if (valid && col0 < p.n) store_chunk16<MODE>(ea, row, col0, v, rowsum);
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -488,6 +429,7 @@ cudaError_t launch_variant(const GemmArgs& g, cudaStream_t s) {
     p.rec = g.ep ? g.ep->rec : nullptr;
     p.zp_c = g.ep ? g.ep->zp_c : 0;
     p.relu = g.ep ? g.ep->relu : 0;
+    p.fast = (g.ep && g.ep->fast_f32) ? 1 : 0;
     p.bias_add = g.bias_add;
     p.c = g.c;
     p.ldc = g.ldc;
@@ -596,6 +538,7 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
         }
         return launch_modes<32, 1, 10>(g, s);
     }
+    if (tc2_supported(g)) return launch_gemm_tc2(g, s);  // CTA-pair 256x256 tiles
     return launch_modes<256, 1, 4>(g, s);
 }
 

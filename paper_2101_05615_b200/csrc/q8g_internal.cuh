@@ -180,6 +180,8 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s);
 bool tc_supported(const GemmArgs& g);
 bool splitk_supported(const GemmArgs& g);
 cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s);
+bool tc2_supported(const GemmArgs& g);
+cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s);
 int tc_trace_copy(unsigned long long* out, int max_ctas);
 
 struct ConvArgs {

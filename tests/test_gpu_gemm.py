@@ -323,3 +323,26 @@ def test_launch_counter_moves(cuda, orc):
     before = q8.launch_count()
     run_raw(np.ones((4, 16), np.uint8), q8.prepack_weights(np.ones((16, 4), np.int8)))
     assert q8.launch_count() > before
+
+
+def test_large_m_pair_kernel_repeated_runs_exact(cuda, orc):
+    # CTA-pair kernel (gemm_tc2.cu) at a size with many tiles per pair and
+    # both TMEM accumulators cycling: raw accumulators vs the oracle, then 20
+    # back-to-back requant + row-sum launches that must all equal the oracle
+    # (a cross-CTA ordering race would show up as sporadic mismatches)
+    m = n = k = 2048
+    c = configs.gemm_case(orc, "C1", m, n, k, seed=2048)
+    pw = q8.prepack_weights(c.b)
+    acc = orc.naive_gemm_i32(c.a, c.b)
+    before = q8.launch_stats()["gemm_tc_large_m"]
+    assert (run_raw(c.a, pw) == acc).all()
+    exp = oracle_requant(orc, c, acc, 1)
+    a_dev = dev(c.a)
+    pipe = requant_pipeline(c, k, q8.ROUND_F32_RNE)
+    outs = [torch.empty((m, n), dtype=torch.uint8, device="cuda") for _ in range(20)]
+    for o in outs:
+        q8.execute_gemm(a_dev, pw, o, pipe)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert (o.cpu().numpy() == exp).all(), i
+    assert q8.launch_stats()["gemm_tc_large_m"] == before + 21

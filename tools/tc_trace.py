@@ -58,6 +58,14 @@ def main():
         if len(col):
             print(f"  {nm:10s} min {col.min()/1e3:8.2f} us  med {np.median(col)/1e3:8.2f}  max {col.max()/1e3:8.2f}")
     c0 = t[0, 0]
+    kb6 = allw[8192:8192 + 384].reshape(6, 64)
+    if (kb6[3] > 0).any():  # CTA-pair kernel: 6 columns
+        nk = int((kb6[0] > 0).sum())
+        print("  pair 0 per k-block (us from CTA0 entry): leader issue / past full / past pfull / MMAs issued /"
+              " follower issue / relay sent")
+        for kb in range(nk):
+            print(f"    kb {kb:2d}: " + " ".join(f"{(kb6[w, kb]-c0)/1e3:7.2f}" for w in range(6)))
+        return
     nk = int((kbs[0] > 0).sum())
     print("  CTA0 per k-block (us from its entry): issue / landed / mma-issued")
     for kb in range(nk):
