@@ -250,6 +250,12 @@ int q8g_packed_b_replicate(const q8g_packed_b* src, int device, q8g_packed_b** o
         q8g_free_packed_b(pb);
         return cuda_fail(e, "replicate copy");
     }
+    // packed weights are complete before any kernel can read them (the GEMM
+    // kernels prefetch B ahead of griddepcontrol.wait, gemm_splitk.cu)
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+        q8g_free_packed_b(pb);
+        return cuda_fail(e, "replicate copy");
+    }
     *out = pb;
     return Q8G_OK;
 }

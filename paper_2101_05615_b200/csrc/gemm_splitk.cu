@@ -181,21 +181,38 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
+    // PDL: start streaming the first stages of B before waiting for the
+    // previous grid.  Packed weights are immutable once q8g_pack_b* returned
+    // (it synchronizes), so no kernel in flight can be writing them; A may be
+    // the previous grid's output and is only loaded after griddepcontrol.wait.
+    const int npre = (kb1 - kb0) < STAGES ? (kb1 - kb0) : STAGES;
+    const uint64_t pol_b = ptx::policy_evict_first();  // weights streamed once
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            for (int i = 0; i < npre; ++i) {
+                ptx::mbar_arrive_expect_tx(full_bar(i), A_STAGE + Cfg::B_STAGE);
+                ptx::bulk_load_hint(sB + i * Cfg::B_STAGE, p.pb + ((size_t)(kb0 + i) * p.np + n0) * kKBlock,
+                                    Cfg::B_STAGE, full_bar(i), pol_b);
+            }
+        }
+        __syncwarp();
+    }
     ptx::griddep_wait();  // PDL: the prologue above overlapped the previous grid
     if (threadIdx.x == 0) sk_stamp(p, 1);
 
     if (warp == 0) {
         // whole warp runs the loop; one elected lane issues (ptx::elect_one)
-        const uint64_t pol_b = ptx::policy_evict_first();  // weights streamed once
         int stage = 0;
         uint32_t phase = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
             ptx::mbar_wait(empty_bar(stage), phase ^ 1);
             if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(full_bar(stage), A_STAGE + Cfg::B_STAGE);
+                if (kb - kb0 >= npre) {  // (the first npre stages' B went out before the PDL wait)
+                    ptx::mbar_arrive_expect_tx(full_bar(stage), A_STAGE + Cfg::B_STAGE);
+                    ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE, p.pb + ((size_t)kb * p.np + n0) * kKBlock,
+                                        Cfg::B_STAGE, full_bar(stage), pol_b);
+                }
                 ptx::tma_load_2d(sA + stage * A_STAGE, &tmap_a, kb * kKBlock, m0, full_bar(stage));
-                ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE, p.pb + ((size_t)kb * p.np + n0) * kKBlock,
-                                    Cfg::B_STAGE, full_bar(stage), pol_b);
                 if (kb == kb0) sk_stamp(p, 2);
                 sk_kb(p, 0, kb - kb0);
             }
