@@ -656,6 +656,7 @@ int q8g_dw_filter_create(const int8_t* w_host, int c, const q8g_requant_params* 
             const int64_t ct = b - (int64_t)p->zp_a * wsum[ch] + 9LL * p->zp_a * zw;
             cterm[ch] = (int32_t)(ct + 0x4B400000LL);
             mult[ch] = rec[ch].mf;
+            if (!(mult[ch] < 7.9228163e28f)) ok = false;  // finite, < 2^96: no inf/NaN products
             for (int cls = 1; cls < 16; ++cls) {
                 int64_t s = 0;
                 for (int t = 0; t < 9; ++t) {

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "ptx.cuh"
@@ -38,7 +39,7 @@ namespace {
 constexpr int G = 16;          // channels per group (MMA N)
 constexpr int TAPS = 10;       // 9 taps + one zero-weight tap (K = 160 = 5 x 32)
 constexpr int ROWS = 8;        // output rows per work unit
-constexpr int NBUF = 3;        // halo buffers in flight
+constexpr int NBUF = 6;        // halo buffers in flight (TMA latency ~3.5 us per 16-B-row halo)
 constexpr int MAXW = 254;      // padded width <= 256 (TMA box limit)
 constexpr int EPI_WARPS = 8;
 
@@ -57,6 +58,10 @@ struct DwParams {
     const int32_t* corr;       // [16][c] border-class corrections
     float lo, hi;              // clamp bounds in the pre-zp_c domain
     int32_t zp_c;
+    // 64-channel-block kernel (dwconv_tc64_kernel)
+    int nblk;                  // c / 64
+    int rb2;                   // ceil(h / 2)
+    int units_blk;             // nb * rb2 units per channel block
     uint8_t* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): per-unit stamps of CTA 0, else null
 };
@@ -359,13 +364,266 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     }
 }
 
+
+// ---------------------------------------------------------------- 64-channel blocks
+// The 16-channel kernel above loads its halo as 16-byte TMA box rows
+// (~3 cycles each; 1140 per unit -> ~1.8 us per unit of TMA time, the
+// measured bound).  Here a CTA owns one block of 64 channels for its whole
+// life: the halo is the natural NHWC rows of that block (64-byte TMA rows,
+// SWIZZLE_64B, 456 per unit), and one MMA step is K = 32 channels of ONE tap:
+// the A window of tap t = the halo rows shifted by (t/3)*(W+2) + t%3 - 1,
+// bytes 32j.. of each row (a swizzled K-major descriptor at any row: the
+// tensor core applies the swizzle on absolute smem addresses, see
+// tools/swz_test.cu).  B per (tap, K-group) is block-diagonal [W_t | -zp_w]
+// (N = 64), so D = sum_t x_t*w_t (columns 0-31) and -zp_w*sum_t x_t (32-63).
+constexpr int CB = 64;      // channels per block: halo row bytes (SWIZZLE_64B)
+constexpr int R2 = 2;       // output rows per unit, one 128-position M tile each
+constexpr int NB2 = 4;      // halo buffers
+constexpr int KG = CB / 32; // K-groups of 32 channels
+constexpr int N2 = 64;      // MMA N: 32 outputs + 32 zero-point columns
+
+struct Dw2Layout {
+    int halo_off, halo_stride, b_off, corr_off, mult_off, bar_off, tmemptr_off, total;
+};
+__host__ __device__ inline Dw2Layout dw2_layout(int wp) {
+    Dw2Layout L;
+    L.halo_off = 1024;  // front guard: the first tap's window starts one position early
+    L.halo_stride = align_up((R2 + 2) * wp * CB + 2048, 1024);  // + tail guard (garbage rows run past the end)
+    L.b_off = L.halo_off + NB2 * L.halo_stride;
+    L.corr_off = L.b_off + 9 * KG * 2048;  // B: [tap][K-group][K half][64 rows][16 B]
+    L.mult_off = L.corr_off + 16 * CB * 4;  // [16 classes][64] int32: cterm + border correction
+    L.bar_off = L.mult_off + CB * 4;
+    L.tmemptr_off = L.bar_off + (2 * NB2 + 4) * 8;
+    L.total = L.tmemptr_off + 16 + 1024;
+    return L;
+}
+
+__host__ __device__ inline uint64_t kmajor_swz64_desc(uint32_t addr) {
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)4 << 61);  // SWIZZLE_64B, 8-row groups of 512 B
+}
+
+// d = {c[15:0], sat_u8(a), sat_u8(b)} (one I2IP)
+__device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
+    dwconv_tc64_kernel(const __grid_constant__ CUtensorMap tmap_x, const DwParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    const uint32_t base = (raw_addr + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base - raw_addr);
+    const Dw2Layout L = dw2_layout(p.wp);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t bar0 = base + L.bar_off;
+    auto full_bar = [&](int b) { return bar0 + 8u * b; };
+    auto empty_bar = [&](int b) { return bar0 + 8u * (NB2 + b); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * NB2 + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * NB2 + 2 + a); };
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmemptr_off);
+    // this CTA's channel block and its share of the block's units
+    const int cb = blockIdx.x % p.nblk;
+    const int cta_in = blockIdx.x / p.nblk;
+    const int ctas = ((int)gridDim.x - cb + p.nblk - 1) / p.nblk;
+    const int c0 = cb * CB;
+    ptx::griddep_launch_dependents();
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_x);
+        for (int b = 0; b < NB2; ++b) {
+            ptx::mbar_init(full_bar(b), 1);
+            ptx::mbar_init(empty_bar(b), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull_bar(a), 1);
+            ptx::mbar_init(tempty_bar(a), EPI_WARPS);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+    ptx::griddep_wait();
+
+    // ---- B for this channel block, per (tap, K-group): [K half][64 rows][16 B];
+    // row n < 32: w[t][c0 + 32j + n] at K index n; row 32 + n: -zp_w at K index n
+    for (int idx = threadIdx.x; idx < 9 * KG * 128; idx += blockDim.x) {
+        const int t = idx / (KG * 128), rem = idx % (KG * 128);
+        const int j = rem / 128, half = (rem % 128) / 64, n = rem % 64;
+        const int oc = n % 32, ch = c0 + j * 32 + oc;
+        uint32_t v[4] = {0, 0, 0, 0};
+        if (oc / 16 == half) {
+            const uint32_t byte = n < 32 ? (uint32_t)(uint8_t)p.wt[t * p.c + ch] : (uint32_t)(uint8_t)(int8_t)(-p.zpw[ch]);
+            v[(oc % 16) / 4] = byte << (8 * (oc % 4));
+        }
+        *reinterpret_cast<uint4*>(smem + L.b_off + (size_t)idx * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    int32_t* corr_s = reinterpret_cast<int32_t*>(smem + L.corr_off);
+    for (int i = threadIdx.x; i < 16 * CB; i += blockDim.x)
+        corr_s[i] = p.corr[(i / CB) * p.c + c0 + i % CB] + p.cterm[c0 + i % CB];
+    float* mult_s = reinterpret_cast<float*>(smem + L.mult_off);
+    for (int i = threadIdx.x; i < CB; i += blockDim.x) mult_s[i] = p.mult[c0 + i];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    for (int b = 0; b < NB2; ++b) {
+        const int hb = (R2 + 2) * p.wp * CB;
+        uint4* g = reinterpret_cast<uint4*>(smem + L.halo_off + b * L.halo_stride + hb);
+        for (int i = threadIdx.x; i < (L.halo_stride - hb) / 16; i += blockDim.x) g[i] = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_ptr;
+    const uint32_t halo_bytes = (uint32_t)((R2 + 2) * p.wp * CB);
+
+    if (warp == 0) {
+        // ------------------------------------------------ halo producer
+        int b = 0;
+        uint32_t ph = 0;
+        for (int k = cta_in; k < p.units_blk; k += ctas) {
+            const int n = k / p.rb2, rb = k % p.rb2;
+            ptx::mbar_wait(empty_bar(b), ph ^ 1);
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(full_bar(b), halo_bytes);
+                // box {64 ch, W+2 px, R2+2 rows, 1} at (c0, col -1, row rb*R2-1, image n)
+                tma_load_4d(base + L.halo_off + b * L.halo_stride, &tmap_x, c0, -1, rb * R2 - 1, n, full_bar(b));
+                dw_stamp(p, 0, (k - cta_in) / ctas);
+            }
+            __syncwarp();
+            if (++b == NB2) {
+                b = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = ptx::idesc_u8s8_s32<128, N2>();
+        // A templates relative to halo position -1: tile r, tap t starts at
+        // position (r + t/3)*(W+2) + t%3 - 1 (the +1 shift keeps fields >= 0)
+        uint64_t a_t[R2 * 9], b_t[9 * KG];
+#pragma unroll
+        for (int r = 0; r < R2; ++r)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) a_t[r * 9 + t] = kmajor_swz64_desc((uint32_t)(((r + t / 3) * p.wp + t % 3) * CB));
+#pragma unroll
+        for (int i = 0; i < 9 * KG; ++i)
+            b_t[i] = kmajor_noswz_desc(base + L.b_off + (uint32_t)(i * 2048), 1024, 128);
+        int b = 0, acc = 0;
+        uint32_t ph = 0, aph = 0;
+        for (int k = cta_in; k < p.units_blk; k += ctas) {
+            ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
+            ptx::mbar_wait(full_bar(b), ph);
+            ptx::tc_fence_after();
+            const uint64_t halo16 = (base + L.halo_off + b * L.halo_stride - (uint32_t)CB) >> 4;
+            if (ptx::elect_one()) {
+                dw_stamp(p, 1, (k - cta_in) / ctas);
+#pragma unroll
+                for (int r = 0; r < R2; ++r)
+#pragma unroll
+                    for (int j = 0; j < KG; ++j) {
+                        const uint32_t d = tmem_base + (uint32_t)(acc * 256 + (r * KG + j) * N2);
+#pragma unroll
+                        for (int t = 0; t < 9; ++t)
+                            ptx::mma_i8(d, a_t[r * 9 + t] + halo16 + (uint64_t)(j * 2), b_t[t * KG + j], idesc, t != 0);
+                    }
+                ptx::tc_commit(empty_bar(b));
+                ptx::tc_commit(tfull_bar(acc));
+                dw_stamp(p, 2, (k - cta_in) / ctas);
+            }
+            __syncwarp();
+            if (++b == NB2) {
+                b = 0;
+                ph ^= 1;
+            }
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ requant epilogue
+        // warpgroup r = output row r of the unit; thread = one position
+        const int ew = warp - 4, r = ew / 4, quarter = ew % 4;
+        const int m = quarter * 32 + lane, ocol = m - 1;
+        const float magic = 12582912.0f;  // 1.5 * 2^23 (cterm carries its bit pattern)
+        const float floor_x = p.lo == 0.0f ? 0.0f : -8388608.0f;  // ReLU: 0; else -2^23 (see conv_tc.cu)
+        const int32_t zoff = 0x4B400000 - p.zp_c;
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int k = cta_in; k < p.units_blk; k += ctas) {
+            const int n = k / p.rb2, oh = (k % p.rb2) * R2 + r;
+            const bool valid = oh < p.h && ocol >= 0 && ocol < p.w;
+            const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
+            ptx::mbar_wait(tfull_bar(acc), aph);
+            ptx::tc_fence_after();
+            if (ew == 0 && lane == 0) dw_stamp(p, 3, (k - cta_in) / ctas);
+            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + r * KG * N2);
+            uint8_t* dst = p.y + ((((size_t)n * p.h + oh) * p.w + ocol) * p.c + c0);
+#pragma unroll
+            for (int j = 0; j < KG; ++j) {
+                uint32_t vw[32], vz[32];
+                ptx::tmem_ld_32x32b_x32(lane_base + (uint32_t)(j * N2), vw);
+                ptx::tmem_ld_32x32b_x32(lane_base + (uint32_t)(j * N2 + 32), vz);
+                ptx::tmem_ld_wait();
+                const int4* cq = reinterpret_cast<const int4*>(corr_s + cls * CB + j * 32);
+                const float4* mq = reinterpret_cast<const float4*>(mult_s + j * 32);
+                uint32_t w8[8];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const int4 cc = cq[g];
+                    const float4 mm = mq[g];
+                    const int32_t cv[4] = {cc.x, cc.y, cc.z, cc.w};
+                    const float mv[4] = {mm.x, mm.y, mm.z, mm.w};
+                    int32_t rr[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        // exact int -> float via the magic bits (|adj| < 2^22, checked at filter creation)
+                        const int32_t bits = (int32_t)(vw[4 * g + e] + vz[4 * g + e]) + cv[e];
+                        float x = __fmul_rn(__fsub_rn(__int_as_float(bits), magic), mv[e]);
+                        x = fmaxf(x, floor_x);
+                        rr[e] = __float_as_int(__fadd_rn(x, magic)) - zoff;
+                    }
+                    w8[g] = pack_sat_u8(rr[1], rr[0], pack_sat_u8(rr[3], rr[2], 0u));
+                }
+                if (valid) {
+                    reinterpret_cast<uint4*>(dst + j * 32)[0] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+                    reinterpret_cast<uint4*>(dst + j * 32)[1] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+            if (ew == 0 && lane == 0) dw_stamp(p, 4, (k - cta_in) / ctas);
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    }
+
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem_base);
+    }
+}
+
+bool dw_tc64_ok(int w, int c) {
+    static const bool off = getenv("Q8G_DW_TC16") != nullptr;  // A/B switch: force the 16-channel kernel
+    return !off && c % CB == 0 && w + 2 <= 128 && dw2_layout(w + 2).total <= 232448;
+}
+
 }  // namespace
 
 bool dw_tc_supported(int h, int w, int c, int32_t zp_a) {
     (void)zp_a;
+    if (h < 1 || tmap_encoder() == nullptr) return false;
+    if (dw_tc64_ok(w, c)) return true;
     // one unit's tiles (ROWS rows of w+2 positions) must fit a 128-column TMEM buffer
-    return c % G == 0 && w + 2 <= MAXW && (ROWS * (w + 2) + 127) / 128 * G <= 128 && h >= 1 &&
-           tmap_encoder() != nullptr &&
+    return c % G == 0 && w + 2 <= MAXW && (ROWS * (w + 2) + 127) / 128 * G <= 128 &&
            dw_layout((ROWS + 2) * (w + 2) * G, c / G).total <= 232448;
 }
 
@@ -373,14 +631,15 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
                                 cudaStream_t s) {
     auto enc = tmap_encoder();
     if (!enc) return cudaErrorNotSupported;
+    const bool tc64 = dw_tc64_ok(w, c);
     CUtensorMap tmap;
     cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)nb};
     cuuint64_t strides[3] = {(cuuint64_t)c, (cuuint64_t)w * c, (cuuint64_t)h * w * c};
-    cuuint32_t box[4] = {(cuuint32_t)G, (cuuint32_t)(w + 2), (cuuint32_t)(ROWS + 2), 1};
+    cuuint32_t box[4] = {(cuuint32_t)(tc64 ? CB : G), (cuuint32_t)(w + 2), (cuuint32_t)((tc64 ? R2 : ROWS) + 2), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(x), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            CU_TENSOR_MAP_INTERLEAVE_NONE, tc64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     DwParams p;
     p.nb = nb;
@@ -403,10 +662,29 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
     p.zp_c = f->zp_c;
     p.y = y;
     p.trace = tc_trace_buffer_ptr();
-    const DwLayout L = dw_layout(p.halo_bytes, p.groups);
-    static bool attr_set[64] = {false};
+    p.nblk = c / CB;
+    p.rb2 = (h + R2 - 1) / R2;
+    p.units_blk = nb * p.rb2;
     int dev = 0;
     cudaGetDevice(&dev);
+    if (tc64) {
+        static bool attr64[64] = {false};
+        if (dev < 64 && !attr64[dev]) {
+            cudaError_t e = cudaFuncSetAttribute(dwconv_tc64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+            if (e != cudaSuccess) return e;
+            attr64[dev] = true;
+        }
+        // whole channel blocks per CTA: grid a multiple of the block count
+        int per_blk = sm_count(dev) / p.nblk;
+        if (per_blk < 1) per_blk = 1;
+        if (per_blk > p.units_blk) per_blk = p.units_blk;
+        const cudaError_t e = launch_with_pdl(dwconv_tc64_kernel, dim3(per_blk * p.nblk), dim3(128 + 32 * EPI_WARPS),
+                                              dw2_layout(p.wp).total, s, tmap, p);
+        count_launch(kFamDwTc);
+        return e;
+    }
+    const DwLayout L = dw_layout(p.halo_bytes, p.groups);
+    static bool attr_set[64] = {false};
     if (dev < 64 && !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(dwconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         if (e != cudaSuccess) return e;
