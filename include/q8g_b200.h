@@ -35,6 +35,7 @@ typedef struct q8g_packed_b q8g_packed_b;     /* PackedWeight (pack.hpp:63-79) *
 typedef struct q8g_epilogue q8g_epilogue;     /* folded OutputPipeline (pipeline.hpp:57-128) */
 typedef struct q8g_kernel_cache q8g_kernel_cache; /* KernelCache (dispatch.hpp:92-146) */
 typedef struct q8g_dw_filter q8g_dw_filter;   /* new: prepacked depthwise filter */
+typedef struct q8g_sparse_csc q8g_sparse_csc; /* SparseWeightCSC (sparse.hpp:13-21) on a device */
 
 /* BlockingParams (pack.hpp:15-38).  Kept for API compatibility: the packed
  * layout is the tcgen05 K-major 128B-swizzled layout whatever the blocking. */
@@ -64,7 +65,7 @@ int q8g_version(void);
 uint64_t q8g_launch_count(void);
 /* per kernel family: [0] pack, [1] GEMM CUDA-core, [2] GEMM tcgen05 small-M,
  * [3] GEMM tcgen05 large-M, [4] conv CUDA-core, [5] conv tcgen05,
- * [6] depthwise CUDA-core, [7] depthwise tcgen05 */
+ * [6] depthwise CUDA-core, [7] depthwise tcgen05, [8] general-pipeline post */
 int q8g_launch_stats(uint64_t* counts, int n);
 /* debug (env Q8G_TC_TRACE set): 8 globaltimer stamps per CTA of the last
  * tensor-core GEMM launch; returns the number of CTA records copied.  With
@@ -135,6 +136,46 @@ int q8g_gemm_u8s8_requant_host(const uint8_t* a_host, int m, int k, int lda,
 int q8g_gemm_u8s8_raw_i32_host(const uint8_t* a_host, int m, int k, int lda,
                                const q8g_packed_b* pb, int32_t* c_host, int ldc, int row_begin,
                                int row_end, void* stream);
+
+/* ---- outlier split + general output pipeline ----
+ * split_outliers (sparse.hpp:33-58), host side: entries with |v| >= threshold
+ * go to a CSC store with their full value (column-major walk), the rest stay
+ * in dense (k x n, ldd).  CSC arrays are caller buffers of capacity cap
+ * (col_ptr n+1 entries); *nnz_out = the outlier count (Q8G_EINVAL if it
+ * exceeds cap: call with cap 0 first to size).  Errors follow the
+ * reference: threshold >= 1, non-empty matrix. */
+int q8g_split_outliers(const int8_t* b_host, int k, int n, int ldb, int threshold, int8_t* dense_host, int ldd,
+                       int32_t* col_ptr, int32_t* row_idx, int8_t* values, int cap, int* nnz_out);
+/* SparseWeightCSC (sparse.hpp:13-21) uploaded to `device` (validated:
+ * col_ptr nondecreasing from 0 to nnz, row_idx in [0,k) and strictly
+ * increasing within a column) */
+int q8g_sparse_csc_create(const int32_t* col_ptr_host, const int32_t* row_idx_host, const int8_t* values_host,
+                          int nnz, int k, int n, int device, q8g_sparse_csc** out);
+int q8g_sparse_csc_free(q8g_sparse_csc* sp);
+
+enum { Q8G_WRITE_RAW_I32 = 0, Q8G_WRITE_REQUANT_U8 = 1, Q8G_WRITE_DEQUANT_F32 = 2 };
+typedef struct q8g_pipeline_args {
+    const q8g_sparse_csc* sparse;  /* SpMDMAdd stage (pipeline.hpp:23-25) or NULL */
+    const int32_t* bias_add_dev;   /* summed BiasAdd stages (N int32, device) for the raw /
+                                      dequant writers, or NULL; the requant writer takes
+                                      them folded into its epilogue (q8g_epilogue_create) */
+    int writer;                    /* Q8G_WRITE_* */
+    const q8g_epilogue* ep;        /* Q8G_WRITE_REQUANT_U8 ([ReluQuantized] Requantize) */
+    double dq_scale;               /* Q8G_WRITE_DEQUANT_F32: QuantParams (quant.hpp:18-21) */
+    int32_t dq_zero_point;
+} q8g_pipeline_args;
+/* execute_gemm with the general pipeline [SpMDMAdd] [BiasAdd]* [ReluQuantized]
+ * writer (pipeline.hpp:157-207).  c_dev is int32 / u8 / float per the writer
+ * (ldc in elements).  The dense product runs on the tensor-core kernels. */
+int q8g_gemm_u8s8_pipeline(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                           const q8g_pipeline_args* pl, void* c_dev, int ldc, int row_begin, int row_end,
+                           q8g_kernel_cache* cache, void* stream);
+/* host views (the reference convention), synchronous: A rows and C rows of
+ * the stripe are staged through the device; bias_add_host replaces
+ * pl->bias_add_dev (which must be NULL) */
+int q8g_gemm_u8s8_pipeline_host(const uint8_t* a_host, int m, int k, int lda, const q8g_packed_b* pb,
+                                const q8g_pipeline_args* pl, const int32_t* bias_add_host, void* c_host, int ldc,
+                                int row_begin, int row_end, void* stream);
 
 /* ---- conv 3x3, stride 1, pad 1, NHWC (new) ----
  * x: [nb][h][w][c] u8 (device), padding value = zp_a of the epilogue.

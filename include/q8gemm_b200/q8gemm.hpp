@@ -20,6 +20,7 @@
 #include <map>
 #include <type_traits>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -191,6 +192,65 @@ struct RequantParams {
     Rounding rounding = Rounding::kRef;
 };
 
+struct QuantParams {  // quant.hpp:18-21
+    double scale = 1.0;
+    int32_t zero_point = 0;
+};
+
+// sparse.hpp:13-21 (host arrays; uploaded once per device on first use)
+struct SparseWeightCSC {
+    std::vector<int32_t> col_ptr;  // n_total + 1, nondecreasing
+    std::vector<int32_t> row_idx;  // strictly increasing within each column
+    std::vector<int8_t> values;
+    int k_total = 0;
+    int n_total = 0;
+    int nnz() const { return static_cast<int>(values.size()); }
+    q8g_sparse_csc* device(int dev) const {  // thread-safe: workers may race on first use
+        std::lock_guard<std::mutex> lock(*mu_);
+        auto it = dev_.find(dev);
+        if (it != dev_.end()) return it->second.get();
+        q8g_sparse_csc* h = nullptr;
+        check(q8g_sparse_csc_create(col_ptr.data(), row_idx.empty() ? nullptr : row_idx.data(),
+                                    values.empty() ? nullptr : values.data(), nnz(), k_total, n_total, dev, &h));
+        dev_.emplace(dev, std::shared_ptr<q8g_sparse_csc>(h, &q8g_sparse_csc_free));
+        return h;
+    }
+
+private:
+    std::shared_ptr<std::mutex> mu_ = std::make_shared<std::mutex>();
+    mutable std::map<int, std::shared_ptr<q8g_sparse_csc>> dev_;
+};
+
+struct SplitWeight {  // sparse.hpp:23-29
+    Matrix<int8_t> dense_small;
+    SparseWeightCSC sparse;
+    int threshold = 0;
+};
+
+// sparse.hpp:33-58: B = dense_small + outliers (|v| >= threshold, CSC)
+inline SplitWeight split_outliers(MatrixView<const int8_t> b, int threshold) {
+    int nnz = 0;
+    check(q8g_split_outliers(b.data, b.rows, b.cols, b.ld, threshold, nullptr, b.cols, nullptr, nullptr, nullptr, 0,
+                             &nnz));
+    SplitWeight sw;
+    sw.threshold = threshold;
+    sw.dense_small = Matrix<int8_t>(b.rows, b.cols);
+    sw.sparse.k_total = b.rows;
+    sw.sparse.n_total = b.cols;
+    sw.sparse.col_ptr.assign(b.cols + 1, 0);
+    sw.sparse.row_idx.assign(std::max(nnz, 1), 0);
+    sw.sparse.values.assign(std::max(nnz, 1), 0);
+    check(q8g_split_outliers(b.data, b.rows, b.cols, b.ld, threshold, sw.dense_small.data(), b.cols,
+                             sw.sparse.col_ptr.data(), sw.sparse.row_idx.data(), sw.sparse.values.data(),
+                             std::max(nnz, 1), &nnz));
+    sw.sparse.row_idx.resize(nnz);
+    sw.sparse.values.resize(nnz);
+    return sw;
+}
+
+struct SpMDMAdd {  // pipeline.hpp:23-25
+    const SparseWeightCSC* sparse = nullptr;
+};
 struct BiasAdd {  // pipeline.hpp:27-29
     std::vector<int32_t> bias;
 };
@@ -200,9 +260,12 @@ struct Requantize {       // pipeline.hpp:33-36
     const std::vector<int32_t>* col_offsets = nullptr;  // nullptr -> the packed weight's own
 };
 struct WriteRawI32 {};  // pipeline.hpp:38
+struct WriteDequantF32 {  // pipeline.hpp:40-42: scale * (acc - zero_point)
+    QuantParams c_params;
+};
 
-using OutputStage = std::variant<BiasAdd, ReluQuantized, Requantize, WriteRawI32>;
-enum class WriterKind { kRawI32, kRequantizeU8 };
+using OutputStage = std::variant<SpMDMAdd, BiasAdd, ReluQuantized, Requantize, WriteRawI32, WriteDequantF32>;
+enum class WriterKind { kRawI32, kRequantizeU8, kDequantF32 };
 
 class OutputPipeline {
 public:
@@ -213,7 +276,8 @@ public:
     static std::optional<std::string> validate(const std::vector<OutputStage>& stages) {
         if (stages.empty()) return std::string("pipeline is empty; a terminal writer stage is required");
         auto is_writer = [](const OutputStage& s) {
-            return std::holds_alternative<Requantize>(s) || std::holds_alternative<WriteRawI32>(s);
+            return std::holds_alternative<Requantize>(s) || std::holds_alternative<WriteRawI32>(s) ||
+                   std::holds_alternative<WriteDequantF32>(s);
         };
         for (std::size_t i = 0; i + 1 < stages.size(); ++i)
             if (is_writer(stages[i]))
@@ -225,6 +289,8 @@ public:
                 const bool ok = i + 2 == stages.size() && std::holds_alternative<Requantize>(stages.back());
                 if (!ok) return std::string("ReluQuantized must immediately precede a Requantize writer");
             }
+            if (const auto* sp = std::get_if<SpMDMAdd>(&stages[i]))
+                if (sp->sparse == nullptr) return std::string("SpMDMAdd requires a sparse matrix");
             if (const auto* rq = std::get_if<Requantize>(&stages[i])) {
                 const RequantParams& p = rq->params;
                 if (!(p.multiplier > 0) && p.multiplier_f32_per_channel.empty() && p.multiplier_per_channel.empty())
@@ -236,7 +302,30 @@ public:
     }
     const std::vector<OutputStage>& stages() const { return stages_; }
     WriterKind writer() const {
-        return std::holds_alternative<WriteRawI32>(stages_.back()) ? WriterKind::kRawI32 : WriterKind::kRequantizeU8;
+        if (std::holds_alternative<WriteRawI32>(stages_.back())) return WriterKind::kRawI32;
+        if (std::holds_alternative<Requantize>(stages_.back())) return WriterKind::kRequantizeU8;
+        return WriterKind::kDequantF32;
+    }
+    const SparseWeightCSC* sparse() const {
+        for (const auto& s : stages_)
+            if (const auto* sp = std::get_if<SpMDMAdd>(&s)) return sp->sparse;
+        return nullptr;
+    }
+    // an SpMDMAdd stage or the WriteDequantF32 writer: the general path (post.cu)
+    bool general() const { return sparse() != nullptr || writer() == WriterKind::kDequantF32; }
+    // the C-ABI description of the general pipeline (bias_add / ep filled by the caller)
+    q8g_pipeline_args args(int device) const {
+        q8g_pipeline_args pa{};
+        const SparseWeightCSC* sp = sparse();
+        pa.sparse = sp ? sp->device(device) : nullptr;
+        pa.writer = writer() == WriterKind::kRawI32        ? Q8G_WRITE_RAW_I32
+                    : writer() == WriterKind::kRequantizeU8 ? Q8G_WRITE_REQUANT_U8
+                                                            : Q8G_WRITE_DEQUANT_F32;
+        if (const auto* dq = std::get_if<WriteDequantF32>(&stages_.back())) {
+            pa.dq_scale = dq->c_params.scale;
+            pa.dq_zero_point = dq->c_params.zero_point;
+        }
+        return pa;
     }
     bool needs_row_offsets() const {  // pipeline.hpp:114-119
         if (const auto* rq = std::get_if<Requantize>(&stages_.back())) {
@@ -260,7 +349,8 @@ public:
         return acc;
     }
     // folded device epilogue for one packed weight (cached; the pipeline is immutable)
-    q8g_epilogue* epilogue(const PackedWeight& pw) const {
+    q8g_epilogue* epilogue(const PackedWeight& pw) const {  // thread-safe: workers share the pipeline
+        std::lock_guard<std::mutex> lock(*mu_);
         auto it = eps_.find(pw.handle());
         if (it != eps_.end()) return it->second.get();
         const auto& rq = std::get<Requantize>(stages_.back());
@@ -298,6 +388,7 @@ public:
 
 private:
     std::vector<OutputStage> stages_;
+    std::shared_ptr<std::mutex> mu_ = std::make_shared<std::mutex>();
     mutable std::map<q8g_packed_b*, std::shared_ptr<q8g_epilogue>> eps_;
     mutable std::vector<PackedWeight> keep_;
 };
@@ -310,7 +401,8 @@ constexpr int kTileRows = 128;  // stripe granularity: one tcgen05 M tile
 template <typename OutT>
 void check_writer_matches(const OutputPipeline& p) {  // pipeline.hpp:142-151
     const bool ok = (std::is_same<OutT, int32_t>::value && p.writer() == WriterKind::kRawI32) ||
-                    (std::is_same<OutT, uint8_t>::value && p.writer() == WriterKind::kRequantizeU8);
+                    (std::is_same<OutT, uint8_t>::value && p.writer() == WriterKind::kRequantizeU8) ||
+                    (std::is_same<OutT, float>::value && p.writer() == WriterKind::kDequantF32);
     if (!ok) throw std::invalid_argument("pipeline writer does not match the output element type");
 }
 
@@ -349,12 +441,22 @@ void execute_gemm(MatrixView<const uint8_t> a, const PackedWeight& pw, MatrixVie
     detail::validate<OutT>(a, pw, out, pipeline, variant, thread_id, num_threads);
     const auto r = detail::stripe_rows<int>(a.rows, thread_id, num_threads);
     if (r.first >= r.second) return;
+    if (pipeline.general() || (std::is_same<OutT, int32_t>::value && !pipeline.bias_add(pw.n_total).empty())) {
+        // [SpMDMAdd] [BiasAdd]* writer (pipeline.hpp:157-207), staged synchronously
+        q8g_pipeline_args pa = pipeline.args(pw.device);
+        std::vector<int32_t> ba;
+        if (pipeline.writer() == WriterKind::kRequantizeU8)
+            pa.ep = pipeline.epilogue(pw);  // BiasAdd folded into the epilogue table
+        else
+            ba = pipeline.bias_add(pw.n_total);
+        check(q8g_gemm_u8s8_pipeline_host(a.data, a.rows, a.cols, a.ld, pw.handle(), &pa, ba.empty() ? nullptr : ba.data(),
+                                          out.data, out.ld, r.first, r.second, nullptr));
+        return;
+    }
     if constexpr (std::is_same<OutT, int32_t>::value) {
-        if (!pipeline.bias_add(pw.n_total).empty())
-            throw std::runtime_error("BiasAdd with WriteRawI32 needs device views");
         check(q8g_gemm_u8s8_raw_i32_host(a.data, a.rows, a.cols, a.ld, pw.handle(), out.data, out.ld, r.first,
                                          r.second, nullptr));
-    } else {
+    } else if constexpr (std::is_same<OutT, uint8_t>::value) {
         check(q8g_gemm_u8s8_requant_host(a.data, a.rows, a.cols, a.ld, pw.handle(), pipeline.epilogue(pw), out.data,
                                          out.ld, r.first, r.second, nullptr));
     }
@@ -369,10 +471,21 @@ void execute_gemm(DeviceView<const uint8_t> a, const PackedWeight& pw, DeviceVie
     const auto r = detail::stripe_rows<int>(a.rows, thread_id, num_threads);
     if (r.first >= r.second) return;
     q8g_kernel_cache* kc = cache ? cache->handle() : nullptr;
+    if (pipeline.general()) {
+        // [SpMDMAdd] [BiasAdd]* writer; BiasAdd: bias_add_dev (raw / dequant) or the epilogue (requant)
+        q8g_pipeline_args pa = pipeline.args(pw.device);
+        if (pipeline.writer() == WriterKind::kRequantizeU8)
+            pa.ep = pipeline.epilogue(pw);
+        else
+            pa.bias_add_dev = bias_add_dev;
+        check(q8g_gemm_u8s8_pipeline(a.data, a.rows, a.cols, a.ld, pw.handle(), &pa, out.data, out.ld, r.first,
+                                     r.second, kc, stream));
+        return;
+    }
     if constexpr (std::is_same<OutT, int32_t>::value) {
         check(q8g_gemm_u8s8_raw_i32(a.data, a.rows, a.cols, a.ld, pw.handle(), bias_add_dev, out.data, out.ld,
                                     r.first, r.second, kc, stream));
-    } else {
+    } else if constexpr (std::is_same<OutT, uint8_t>::value) {
         check(q8g_gemm_u8s8_requant(a.data, a.rows, a.cols, a.ld, pw.handle(), pipeline.epilogue(pw), out.data,
                                     out.ld, r.first, r.second, kc, stream));
     }

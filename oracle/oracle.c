@@ -376,3 +376,58 @@ void orc_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c, int32_t zp_a,
     parallel_rows(dw_rows, &g, nb * h * w, threads);
     free(wsum);
 }
+
+/* ---- outlier split + SpMDMAdd + WriteDequantF32 ---- */
+
+/* sparse.hpp:33-58 split_outliers: column-major walk; |v| >= threshold goes to
+ * the CSC part with its full value, the rest stays in dense_small.  Returns
+ * nnz, or -1 if it exceeds cap (the CSC arrays are left partially filled). */
+int orc_split_outliers(const int8_t* b, int k, int n, int ldb, int threshold, int8_t* dense, int ldd,
+                       int32_t* col_ptr, int32_t* row_idx, int8_t* values, int cap) {
+    int nnz = 0;
+    col_ptr[0] = 0;
+    for (int j = 0; j < n; ++j) {
+        for (int kk = 0; kk < k; ++kk) {
+            const int8_t v = b[(size_t)kk * ldb + j];
+            const int av = v < 0 ? -(int)v : (int)v;
+            if (av >= threshold) {
+                if (nnz >= cap) return -1;
+                row_idx[nnz] = kk;
+                values[nnz] = v;
+                ++nnz;
+                dense[(size_t)kk * ldd + j] = 0;
+            } else {
+                dense[(size_t)kk * ldd + j] = v;
+            }
+        }
+        col_ptr[j + 1] = nnz;
+    }
+    return nnz;
+}
+
+/* sparse.hpp:62-80 spmdm_block over the whole matrix: acc[i][j] += sum over
+ * the CSC entries (k, v) of column j of A[i][k] * v (int32, wrapping) */
+void orc_spmdm_add(const uint8_t* a, int m, int k, int lda, const int32_t* col_ptr, const int32_t* row_idx,
+                   const int8_t* values, int n, int32_t* acc, int ldacc) {
+    (void)k;
+    for (int j = 0; j < n; ++j)
+        for (int32_t idx = col_ptr[j]; idx < col_ptr[j + 1]; ++idx) {
+            const int kk = row_idx[idx];
+            const int32_t v = values[idx];
+            for (int i = 0; i < m; ++i) {
+                int32_t* p = &acc[(size_t)i * ldacc + j];
+                *p = (int32_t)((uint32_t)*p + (uint32_t)((int32_t)a[(size_t)i * lda + kk] * v));
+            }
+        }
+}
+
+/* pipeline.hpp:199-207 WriteDequantF32: out = (float)(scale * (acc - zp)),
+ * the int subtraction in 32-bit two's complement (the reference's int
+ * arithmetic as compiled), one fp64 multiply, one RN conversion to float */
+void orc_dequant_f32(const int32_t* acc, int m, int n, int ldacc, double scale, int32_t zp, float* out, int ldo) {
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int32_t d = (int32_t)((uint32_t)acc[(size_t)i * ldacc + j] - (uint32_t)zp);
+            out[(size_t)i * ldo + j] = (float)(scale * (double)d);
+        }
+}

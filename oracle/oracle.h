@@ -103,6 +103,14 @@ void orc_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c, int32_t zp_a,
                    int32_t zp_c, int relu, uint8_t* out, int32_t* acc_out /* may be NULL */,
                    int threads);
 
+/* ---- outlier split (sparse.hpp:33-58), SpMDMAdd (sparse.hpp:62-80),
+ * WriteDequantF32 (pipeline.hpp:199-207) ---- */
+int orc_split_outliers(const int8_t* b, int k, int n, int ldb, int threshold, int8_t* dense, int ldd,
+                       int32_t* col_ptr /* n+1 */, int32_t* row_idx, int8_t* values, int cap);
+void orc_spmdm_add(const uint8_t* a, int m, int k, int lda, const int32_t* col_ptr, const int32_t* row_idx,
+                   const int8_t* values, int n, int32_t* acc, int ldacc);
+void orc_dequant_f32(const int32_t* acc, int m, int n, int ldacc, double scale, int32_t zp, float* out, int ldo);
+
 #ifdef __cplusplus
 }
 #endif

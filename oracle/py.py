@@ -72,6 +72,9 @@ class Oracle:
             "orc_im2col3x3": (None, [_P, _I, _I, _I, _I, C.c_uint8, _P, _I]),
             "orc_conv3x3_i32": (None, [_P, _I, _I, _I, _I, C.c_uint8, _P, _I, _P, _I]),
             "orc_dwconv3x3": (None, [_P, _I, _I, _I, _I, C.c_int32, _P, _P, _P, _P, C.c_int32, _I, _P, _P, _I]),
+            "orc_split_outliers": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _I]),
+            "orc_spmdm_add": (None, [_P, _I, _I, _I, _P, _P, _P, _I, _P, _I]),
+            "orc_dequant_f32": (None, [_P, _I, _I, _I, _D, C.c_int32, _P, _I]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -124,6 +127,36 @@ class Oracle:
         out = np.zeros((m, n), dtype=np.uint8)
         self.L.orc_requant_matrix(_p(acc), m, n, n, _p(rs), _p(cs), zp_a, _p(zpb), 1 if pc else 0, k_total,
                                   _p(bi), rounding, _p(md), _p(mf), zp_c, 1 if relu else 0, _p(out), n)
+        return out
+
+    # ---- outlier split / SpMDMAdd / WriteDequantF32 (sparse.hpp:33-80, pipeline.hpp:199-207)
+    def split_outliers(self, b: np.ndarray, threshold: int):
+        """-> (dense_small, col_ptr, row_idx, values)"""
+        b = np.ascontiguousarray(b, dtype=np.int8)
+        k, n = b.shape
+        dense = np.zeros_like(b)
+        cp = np.zeros(n + 1, dtype=np.int32)
+        ri = np.zeros(k * n, dtype=np.int32)
+        vals = np.zeros(k * n, dtype=np.int8)
+        nnz = self.L.orc_split_outliers(_p(b), k, n, n, threshold, _p(dense), n, _p(cp), _p(ri), _p(vals), k * n)
+        return dense, cp, ri[:nnz].copy(), vals[:nnz].copy()
+
+    def spmdm_add(self, a, col_ptr, row_idx, values, acc):
+        """acc (M x N int32, modified copy) += A x sparse"""
+        a = np.ascontiguousarray(a, dtype=np.uint8)
+        out = np.array(acc, dtype=np.int32, copy=True, order="C")
+        cp = np.ascontiguousarray(col_ptr, dtype=np.int32)
+        ri = np.ascontiguousarray(row_idx, dtype=np.int32)
+        vals = np.ascontiguousarray(values, dtype=np.int8)
+        self.L.orc_spmdm_add(_p(a), a.shape[0], a.shape[1], a.shape[1], _p(cp), _p(ri), _p(vals), out.shape[1],
+                             _p(out), out.shape[1])
+        return out
+
+    def dequant_f32(self, acc, scale: float, zero_point: int):
+        acc = np.ascontiguousarray(acc, dtype=np.int32)
+        out = np.zeros(acc.shape, dtype=np.float32)
+        self.L.orc_dequant_f32(_p(acc), acc.shape[0], acc.shape[1], acc.shape[1], scale, zero_point, _p(out),
+                               acc.shape[1])
         return out
 
     def prepack_ref(self, b: np.ndarray, ncb: int, kcb: int, nr: int) -> np.ndarray:
@@ -242,6 +275,9 @@ class RefLib:
             "refx_requantize_scalar": (_I, [C.c_int32, C.c_int32, C.c_int32, _D, _I, _I, _I, _I, _P, _I, _I]),
             "refx_requantize_adjust": (C.c_longlong, [C.c_int32, C.c_int32, C.c_int32, _I, _I, _I, C.c_int32]),
             "refx_pipeline_validate": (_I, [_P, _I, C.c_char_p, _I]),
+            "refx_split_outliers": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P]),
+            "refx_gemm_pipeline": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _I, _P, _I, _D, _I, _I, _I, _P, _I, _P, _D,
+                                        _I, _P, _I, _I]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -282,6 +318,19 @@ class RefLib:
     def requantize_adjust(self, acc, ro, co, zp_a, zp_b, k_total, bias=0):
         return int(self.L.refx_requantize_adjust(acc, ro, co, zp_a, zp_b, k_total, bias))
 
+    def split_outliers(self, b: np.ndarray, threshold: int):
+        """the reference's split_outliers -> (dense_small, col_ptr, row_idx, values)"""
+        b = np.ascontiguousarray(b, dtype=np.int8)
+        k, n = b.shape
+        dense = np.zeros_like(b)
+        cp = np.zeros(n + 1, dtype=np.int32)
+        ri = np.zeros(k * n, dtype=np.int32)
+        vals = np.zeros(k * n, dtype=np.int8)
+        nnz = C.c_int()
+        self._chk(self.L.refx_split_outliers(_p(b), k, n, n, threshold, _p(dense), _p(cp), _p(ri), _p(vals), k * n,
+                                             C.byref(nnz)))
+        return dense, cp, ri[:nnz.value].copy(), vals[:nnz.value].copy()
+
     def pipeline_validate(self, kinds):
         k = np.asarray(kinds, dtype=np.int32)
         buf = C.create_string_buffer(512)
@@ -317,6 +366,30 @@ class RefPacked:
         out = np.zeros((a.shape[0], self.n), dtype=np.int32)
         self.lib._chk(self.lib.L.refx_gemm_raw(_p(a), a.shape[0], a.shape[1], a.shape[1], self.h, _p(out), self.n,
                                                threads))
+        return out
+
+    def gemm_pipeline(self, a, writer, sparse=None, bias_add=None, mult=1.0, zp_a=0, zp_b=0, zp_c=0, rq_bias=None,
+                      relu=False, col_offsets=None, dq_scale=1.0, dq_zero_point=0, threads=1):
+        """execute_gemm with [SpMDMAdd] [BiasAdd] + writer: 'raw' | 'requant' | 'dequant'.
+        sparse = (col_ptr, row_idx, values) of this packed (dense) weight's outliers."""
+        a = np.ascontiguousarray(a, dtype=np.uint8)
+        m, k = a.shape
+        w = {"raw": 0, "requant": 1, "dequant": 2}[writer]
+        out = np.zeros((m, self.n), dtype={0: np.int32, 1: np.uint8, 2: np.float32}[w])
+        arrs = []
+
+        def arr(x, dt):
+            if x is None:
+                return None
+            v = np.ascontiguousarray(x, dtype=dt)
+            arrs.append(v)
+            return _p(v)
+        cp, ri, vals = sparse if sparse is not None else (None, None, None)
+        nnz = 0 if sparse is None else len(vals)
+        self.lib._chk(self.lib.L.refx_gemm_pipeline(
+            _p(a), m, k, k, self.h, arr(cp, np.int32), arr(ri, np.int32), arr(vals, np.int8), nnz,
+            arr(bias_add, np.int32), w, mult, zp_a, zp_b, zp_c, arr(rq_bias, np.int32), 1 if relu else 0,
+            arr(col_offsets, np.int32), dq_scale, dq_zero_point, out.ctypes.data, self.n, threads))
         return out
 
     def gemm_requant(self, a, mult, zp_a, zp_b, zp_c, bias=None, relu=False, threads=1, out=None):

@@ -10,7 +10,8 @@
 //   execute_gemm      engine.hpp:59-169 (caller-owned threads, as in
 //                     acceptance.cpp:47-61 / test_engine.cpp:17-25)
 //   OutputPipeline    pipeline.hpp:57-128 with Requantize / ReluQuantized /
-//                     WriteRawI32
+//                     WriteRawI32 / WriteDequantF32 / BiasAdd / SpMDMAdd
+//   split_outliers    sparse.hpp:33-58
 //   naive_gemm_i32    oracle.hpp:15-30
 //   requantize_scalar quant.hpp:127-133
 #include <cstdint>
@@ -209,6 +210,81 @@ int refx_pipeline_validate(const int* kinds, int n, char* msg, int msg_len) {
     if (!err) return 0;
     std::snprintf(msg, msg_len, "%s", err->c_str());
     return 22;
+}
+
+// sparse.hpp:33-58 split_outliers; CSC arrays written to caller buffers of
+// capacity cap.  Returns nnz, -1 if it exceeds cap, or 22 on an exception.
+int refx_split_outliers(const int8_t* b, int k, int n, int ldb, int threshold, int8_t* dense, int32_t* col_ptr,
+                        int32_t* row_idx, int8_t* values, int cap, int* nnz_out) {
+    try {
+        const SplitWeight sw = split_outliers(MatrixView<const int8_t>{b, k, n, ldb}, threshold);
+        std::memcpy(dense, sw.dense_small.data(), (size_t)k * n);
+        std::memcpy(col_ptr, sw.sparse.col_ptr.data(), sizeof(int32_t) * (n + 1));
+        *nnz_out = sw.sparse.nnz();
+        if (sw.sparse.nnz() > cap) return -1;
+        std::memcpy(row_idx, sw.sparse.row_idx.data(), sizeof(int32_t) * sw.sparse.nnz());
+        std::memcpy(values, sw.sparse.values.data(), (size_t)sw.sparse.nnz());
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 22;
+    }
+}
+
+// execute_gemm (engine.hpp:59-169) with [SpMDMAdd] [BiasAdd] then a writer:
+// writer 0 WriteRawI32 (int32 out), 1 [ReluQuantized] Requantize (u8 out,
+// col_offsets = the given full-K vector), 2 WriteDequantF32 (float out).
+int refx_gemm_pipeline(const uint8_t* a, int m, int k, int lda, void* h, const int32_t* col_ptr,
+                       const int32_t* row_idx, const int8_t* values, int nnz, const int32_t* bias_add, int writer,
+                       double multiplier, int zp_a, int zp_b, int zp_c, const int32_t* rq_bias, int relu,
+                       const int32_t* col_offsets, double dq_scale, int dq_zero_point, void* out, int ldo,
+                       int threads) {
+    try {
+        MatrixView<const uint8_t> av{a, m, k, lda};
+        const auto& pw = *static_cast<PackedWeight*>(h);
+        const int n = pw.n_total;
+        SparseWeightCSC sp;
+        ColOffsets co;
+        std::vector<OutputStage> stages;
+        if (col_ptr) {
+            sp.k_total = k;
+            sp.n_total = n;
+            sp.col_ptr.assign(col_ptr, col_ptr + n + 1);
+            sp.row_idx.assign(row_idx, row_idx + nnz);
+            sp.values.assign(values, values + nnz);
+            stages.push_back(SpMDMAdd{&sp});
+        }
+        if (bias_add) stages.push_back(BiasAdd{std::span<const int32_t>(bias_add, (size_t)n)});
+        if (writer == 0) {
+            stages.push_back(WriteRawI32{});
+            run_workers(threads, av, pw, MatrixView<int32_t>{static_cast<int32_t*>(out), m, n, ldo},
+                        OutputPipeline(std::move(stages)));
+        } else if (writer == 1) {
+            RequantParams rp;
+            rp.multiplier = multiplier;
+            rp.zp_a = zp_a;
+            rp.zp_b = zp_b;
+            rp.zp_c = zp_c;
+            rp.k_total = k;
+            if (rq_bias) rp.bias.assign(rq_bias, rq_bias + n);
+            co.values.assign(col_offsets, col_offsets + n);
+            if (relu) stages.push_back(ReluQuantized{});
+            stages.push_back(Requantize{rp, &co});
+            run_workers(threads, av, pw, MatrixView<uint8_t>{static_cast<uint8_t*>(out), m, n, ldo},
+                        OutputPipeline(std::move(stages)));
+        } else {
+            QuantParams qp;
+            qp.scale = dq_scale;
+            qp.zero_point = dq_zero_point;
+            stages.push_back(WriteDequantF32{qp});
+            run_workers(threads, av, pw, MatrixView<float>{static_cast<float*>(out), m, n, ldo},
+                        OutputPipeline(std::move(stages)));
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 22;
+    }
 }
 
 }  // extern "C"

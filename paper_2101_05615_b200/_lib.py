@@ -47,6 +47,20 @@ class RequantParamsC(C.Structure):
     ]
 
 
+class PipelineArgsC(C.Structure):  # q8g_pipeline_args
+    _fields_ = [
+        ("sparse", C.c_void_p),
+        ("bias_add_dev", C.c_void_p),
+        ("writer", C.c_int),
+        ("ep", C.c_void_p),
+        ("dq_scale", C.c_double),
+        ("dq_zero_point", C.c_int32),
+    ]
+
+
+Q8G_WRITE_RAW_I32, Q8G_WRITE_REQUANT_U8, Q8G_WRITE_DEQUANT_F32 = 0, 1, 2
+
+
 # (name, restype, argtypes)
 _P = C.c_void_p
 _I = C.c_int
@@ -83,6 +97,10 @@ _SIGS = [
     ("q8g_dw_filter_create", _I, [_P, _I, C.POINTER(RequantParamsC), _I, C.POINTER(_P)]),
     ("q8g_dw_filter_free", _I, [_P]),
     ("q8g_dwconv3x3_u8s8_nhwc", _I, [_P, _I, _I, _I, _I, _P, _P, _I, _I, _P]),
+    ("q8g_split_outliers", _I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _I, C.POINTER(_I)]),
+    ("q8g_sparse_csc_create", _I, [_P, _P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
+    ("q8g_sparse_csc_free", _I, [_P]),
+    ("q8g_gemm_u8s8_pipeline", _I, [_P, _I, _I, _I, _P, C.POINTER(PipelineArgsC), _P, _I, _I, _I, _P, _P]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]
@@ -125,7 +143,7 @@ def launch_count() -> int:
 
 
 FAMILIES = ("pack", "gemm_simt", "gemm_tc_small_m", "gemm_tc_large_m", "conv_simt", "conv_tc", "dw_simt",
-            "dw_tc")
+            "dw_tc", "post")
 
 
 def launch_stats() -> dict:

@@ -208,8 +208,76 @@ class RequantParams:
 
 
 @dataclass
-class SpMDMAdd:  # pipeline.hpp:23-25 -- not on the B200 hot path
-    sparse: object = None
+class QuantParams:  # quant.hpp:18-21
+    scale: float = 1.0      # real units per quantum, > 0
+    zero_point: int = 0
+
+
+@dataclass
+class SparseWeightCSC:
+    """sparse.hpp:13-21: compressed-sparse-column store of the outlier weight
+    entries.  Uploaded to a device on first use (one copy per device)."""
+    col_ptr: np.ndarray          # n_total + 1, nondecreasing
+    row_idx: np.ndarray          # strictly increasing within each column
+    values: np.ndarray           # int8
+    k_total: int = 0
+    n_total: int = 0
+
+    def nnz(self) -> int:
+        return int(len(self.values))
+
+    def _device(self, device: int) -> C.c_void_p:
+        hs = self.__dict__.setdefault("_handles", {})
+        if device not in hs:
+            cp = np.ascontiguousarray(self.col_ptr, dtype=np.int32)
+            ri = np.ascontiguousarray(self.row_idx, dtype=np.int32)
+            va = np.ascontiguousarray(self.values, dtype=np.int8)
+            h = C.c_void_p()
+            check(load().q8g_sparse_csc_create(cp.ctypes.data, ri.ctypes.data if len(ri) else None,
+                                               va.ctypes.data if len(va) else None, len(va), self.k_total,
+                                               self.n_total, device, C.byref(h)))
+            hs[device] = h
+        return hs[device]
+
+    def __del__(self):
+        try:
+            for h in self.__dict__.get("_handles", {}).values():
+                load().q8g_sparse_csc_free(h)
+        except Exception:
+            pass
+
+
+@dataclass
+class SplitWeight:  # sparse.hpp:23-29
+    dense_small: np.ndarray
+    sparse: SparseWeightCSC
+    threshold: int = 0
+
+
+def split_outliers(b, threshold: int) -> SplitWeight:
+    """sparse.hpp:33-58: B = dense_small + sparse, the outliers (|v| >=
+    threshold) kept at full value in a CSC store.  Preprocessing only."""
+    b = np.ascontiguousarray(np.asarray(b), dtype=np.int8)
+    if b.ndim != 2:
+        raise InvalidArgument(_lib.Q8G_EINVAL, "split_outliers: matrix must be non-empty")
+    k, n = b.shape
+    nnz = C.c_int()
+    check(load().q8g_split_outliers(b.ctypes.data, k, n, n, int(threshold), None, n, None, None, None, 0,
+                                    C.byref(nnz)))
+    dense = np.zeros_like(b)
+    cp = np.zeros(n + 1, dtype=np.int32)
+    cap = max(1, nnz.value)
+    ri = np.zeros(cap, dtype=np.int32)
+    va = np.zeros(cap, dtype=np.int8)
+    check(load().q8g_split_outliers(b.ctypes.data, k, n, n, int(threshold), dense.ctypes.data, n, cp.ctypes.data,
+                                    ri.ctypes.data, va.ctypes.data, cap, C.byref(nnz)))
+    sp = SparseWeightCSC(cp, ri[:nnz.value].copy(), va[:nnz.value].copy(), k, n)
+    return SplitWeight(dense, sp, int(threshold))
+
+
+@dataclass
+class SpMDMAdd:  # pipeline.hpp:23-25 (general-pipeline path, post.cu)
+    sparse: Optional[SparseWeightCSC] = None
 
 
 @dataclass
@@ -234,9 +302,8 @@ class WriteRawI32:  # pipeline.hpp:38
 
 
 @dataclass
-class WriteDequantF32:  # pipeline.hpp:40-42 -- not on the B200 hot path
-    scale: float = 1.0
-    zero_point: int = 0
+class WriteDequantF32:  # pipeline.hpp:40-42: out = scale * (acc - zero_point)
+    c_params: QuantParams = field(default_factory=QuantParams)
 
 
 _WRITERS = (Requantize, WriteRawI32, WriteDequantF32)
@@ -298,11 +365,16 @@ class OutputPipeline:
                 acc = b if acc is None else acc + b
         return None if acc is None else acc.astype(np.int32)
 
-    def _unsupported(self):
+    def sparse(self) -> Optional[SparseWeightCSC]:
         for s in self.stages:
-            if isinstance(s, (SpMDMAdd, WriteDequantF32)):
-                raise _lib.Q8GError(_lib.Q8G_ENOTSUP,
-                                    f"{type(s).__name__} is not on the B200 hot path (SURVEY.md §8(f) next)")
+            if isinstance(s, SpMDMAdd):
+                return s.sparse
+        return None
+
+    def general(self) -> bool:
+        """True when the pipeline needs the general path (post.cu): an
+        SpMDMAdd stage or the WriteDequantF32 writer."""
+        return self.sparse() is not None or isinstance(self.stages[-1], WriteDequantF32)
 
     def epilogue(self, pw: PackedWeight) -> C.c_void_p:
         """Fold [BiasAdd]* [ReluQuantized] Requantize into the device table.
@@ -312,7 +384,6 @@ class OutputPipeline:
         hit = cache.get(id(pw))
         if hit is not None and hit[0] is pw:
             return hit[1]
-        self._unsupported()
         rq = self.stages[-1]
         assert isinstance(rq, Requantize)
         p = rq.params
@@ -404,9 +475,9 @@ def execute_gemm(a, pw: PackedWeight, out, pipeline: OutputPipeline,
     w = pipeline.writer()
     out_is_i32 = (out.dtype == torch.int32) if _is_dev(out) else (out.dtype == np.int32)
     out_is_u8 = (out.dtype == torch.uint8) if _is_dev(out) else (out.dtype == np.uint8)
-    if not ((w is WriteRawI32 and out_is_i32) or (w is Requantize and out_is_u8)):
-        if w is WriteDequantF32:
-            pipeline._unsupported()
+    out_is_f32 = (out.dtype == torch.float32) if _is_dev(out) else (out.dtype == np.float32)
+    if not ((w is WriteRawI32 and out_is_i32) or (w is Requantize and out_is_u8) or
+            (w is WriteDequantF32 and out_is_f32)):
         raise InvalidArgument(_lib.Q8G_EINVAL, "pipeline writer does not match the output element type")
     if variant == KernelVariant.kAccI16 and not i16_accumulation_exact(pw.max_abs, pw.blocking.kcb):
         raise InvalidArgument(
@@ -414,9 +485,11 @@ def execute_gemm(a, pw: PackedWeight, out, pipeline: OutputPipeline,
             f"execute_gemm: INT16 accumulation rejected: 255 * max|B| * kcb = {255 * pw.max_abs * pw.blocking.kcb} "
             "exceeds 32767; split outliers with a threshold satisfying 255 * (T - 1) * kcb <= 32767 "
             "(see max_i16_split_threshold)")
-    pipeline._unsupported()
     r0, r1 = stripe_rows(m, thread_id, num_threads)
     if r0 >= r1:
+        return
+    if pipeline.general():
+        _execute_general(a, pw, out, pipeline, r0, r1, cache, stream)
         return
     lib = load()
     cache_h = cache.handle if cache is not None else None
@@ -444,6 +517,53 @@ def execute_gemm(a, pw: PackedWeight, out, pipeline: OutputPipeline,
                                             cache_h, _stream_ptr(stream)))
         else:
             check(lib.q8g_gemm_u8s8_requant_host(_ptr(a), m, k, lda, pw.handle, ep, _ptr(out), ldc, r0, r1, None))
+
+
+def _execute_general(a, pw: PackedWeight, out, pipeline: OutputPipeline, r0: int, r1: int,
+                     cache: Optional[KernelCache], stream) -> None:
+    """[SpMDMAdd] [BiasAdd]* [ReluQuantized] writer (pipeline.hpp:157-207)
+    through q8g_gemm_u8s8_pipeline; host views are staged through the device
+    (the reference's host-view convention, synchronous)."""
+    host = not _is_dev(a)
+    if host != (not _is_dev(out)):
+        raise InvalidArgument(_lib.Q8G_EINVAL, "execute_gemm: A and out must both be device or both host views")
+    dev_index = pw.device
+    if host:
+        a_d = torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev_index}")
+        out_d = torch.empty(out.shape, dtype={np.dtype(np.int32): torch.int32, np.dtype(np.uint8): torch.uint8,
+                                              np.dtype(np.float32): torch.float32}[np.dtype(out.dtype)],
+                            device=f"cuda:{dev_index}")
+    else:
+        a_d, out_d = a, out
+    m, k = a_d.shape
+    n = pw.n_total
+    sp = pipeline.sparse()
+    if sp is not None and (sp.k_total != k or sp.n_total != n):
+        raise InvalidArgument(_lib.Q8G_EINVAL, "spmdm_block: block extents out of bounds")
+    w = pipeline.writer()
+    pa = _lib.PipelineArgsC()
+    pa.sparse = sp._device(dev_index) if sp is not None else None
+    keep = []
+    if w is Requantize:
+        pa.writer = _lib.Q8G_WRITE_REQUANT_U8
+        pa.ep = pipeline.epilogue(pw)  # folds BiasAdd into the table
+    else:
+        pa.writer = _lib.Q8G_WRITE_RAW_I32 if w is WriteRawI32 else _lib.Q8G_WRITE_DEQUANT_F32
+        ba = pipeline.bias_add()
+        if ba is not None:
+            bdev = torch.from_numpy(ba).to(a_d.device)
+            keep.append(bdev)
+            pa.bias_add_dev = bdev.data_ptr()
+        if w is WriteDequantF32:
+            cp = pipeline.stages[-1].c_params
+            pa.dq_scale, pa.dq_zero_point = float(cp.scale), int(cp.zero_point)
+    check(load().q8g_gemm_u8s8_pipeline(a_d.data_ptr(), m, k, _ld(a_d), pw.handle, C.byref(pa), out_d.data_ptr(),
+                                        _ld(out_d), r0, r1, cache.handle if cache is not None else None,
+                                        _stream_ptr(stream)))
+    if host:
+        torch.cuda.synchronize(dev_index)
+        res = out_d[r0:r1].cpu().numpy()
+        out[r0:r1] = res
 
 
 # ---------------------------------------------------------------- conv 3x3

@@ -475,6 +475,196 @@ int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g
                        row_end, cache, (cudaStream_t)stream, true);
 }
 
+// ---------------------------------------------------------------- outliers + general pipeline
+
+int q8g_split_outliers(const int8_t* b, int k, int n, int ldb, int threshold, int8_t* dense, int ldd,
+                       int32_t* col_ptr, int32_t* row_idx, int8_t* values, int cap, int* nnz_out) {
+    if (threshold < 1) return fail(Q8G_EINVAL, "split_outliers: threshold must be >= 1");
+    if (k < 1 || n < 1) return fail(Q8G_EINVAL, "split_outliers: matrix must be non-empty");
+    if (!b || !nnz_out || ldb < n || (dense && ldd < n) || (cap > 0 && (!col_ptr || !row_idx || !values)))
+        return fail(Q8G_EINVAL, "split_outliers: bad arguments");
+    // sparse.hpp:46-56: column-major walk builds the CSC arrays directly
+    int nnz = 0;
+    if (col_ptr && cap > 0) col_ptr[0] = 0;
+    for (int j = 0; j < n; ++j) {
+        for (int kk = 0; kk < k; ++kk) {
+            const int8_t v = b[(size_t)kk * ldb + j];
+            const bool outlier = (v < 0 ? -(int)v : (int)v) >= threshold;
+            if (dense) dense[(size_t)kk * ldd + j] = outlier ? 0 : v;
+            if (outlier) {
+                if (nnz < cap) {
+                    row_idx[nnz] = kk;
+                    values[nnz] = v;
+                }
+                ++nnz;
+            }
+        }
+        if (col_ptr && cap > 0) col_ptr[j + 1] = nnz;
+    }
+    *nnz_out = nnz;
+    if (cap > 0 && nnz > cap) return fail(Q8G_EINVAL, "split_outliers: more outliers than the CSC capacity");
+    return Q8G_OK;
+}
+
+int q8g_sparse_csc_create(const int32_t* col_ptr, const int32_t* row_idx, const int8_t* values, int nnz, int k,
+                          int n, int device, q8g_sparse_csc** out) {
+    if (!out || !col_ptr || k < 1 || n < 1 || nnz < 0 || (nnz > 0 && (!row_idx || !values)))
+        return fail(Q8G_EINVAL, "SparseWeightCSC: bad arguments");
+    *out = nullptr;
+    if (col_ptr[0] != 0 || col_ptr[n] != nnz) return fail(Q8G_EINVAL, "SparseWeightCSC: col_ptr must run 0..nnz");
+    for (int j = 0; j < n; ++j) {
+        if (col_ptr[j + 1] < col_ptr[j]) return fail(Q8G_EINVAL, "SparseWeightCSC: col_ptr must be nondecreasing");
+        for (int32_t i = col_ptr[j]; i < col_ptr[j + 1]; ++i) {
+            if (row_idx[i] < 0 || row_idx[i] >= k) return fail(Q8G_EINVAL, "SparseWeightCSC: row index out of range");
+            if (i > col_ptr[j] && row_idx[i] <= row_idx[i - 1])
+                return fail(Q8G_EINVAL, "SparseWeightCSC: row indices must increase within a column");
+        }
+    }
+    DeviceGuard dg(device);
+    auto* sp = new (std::nothrow) q8g_sparse_csc();
+    if (!sp) return fail(Q8G_ENOMEM, "out of host memory");
+    sp->device = device;
+    sp->k = k;
+    sp->n = n;
+    sp->nnz = nnz;
+    cudaError_t e;
+    if ((e = cudaMalloc(&sp->col_ptr, sizeof(int32_t) * (n + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&sp->row_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1))) != cudaSuccess ||
+        (e = cudaMalloc(&sp->values, nnz > 0 ? nnz : 1)) != cudaSuccess ||
+        (e = cudaMemcpy(sp->col_ptr, col_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (nnz > 0 && (e = cudaMemcpy(sp->row_idx, row_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice)) !=
+                        cudaSuccess) ||
+        (nnz > 0 && (e = cudaMemcpy(sp->values, values, nnz, cudaMemcpyHostToDevice)) != cudaSuccess)) {
+        q8g_sparse_csc_free(sp);
+        return cuda_fail(e, "SparseWeightCSC upload");
+    }
+    *out = sp;
+    return Q8G_OK;
+}
+
+int q8g_sparse_csc_free(q8g_sparse_csc* sp) {
+    if (!sp) return Q8G_OK;
+    DeviceGuard dg(sp->device);
+    if (sp->col_ptr) cudaFree(sp->col_ptr);
+    if (sp->row_idx) cudaFree(sp->row_idx);
+    if (sp->values) cudaFree(sp->values);
+    delete sp;
+    return Q8G_OK;
+}
+
+int q8g_gemm_u8s8_pipeline(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                           const q8g_pipeline_args* pl, void* c_dev, int ldc, int row_begin, int row_end,
+                           q8g_kernel_cache* cache, void* stream) {
+    if (!pl || !pb) return fail(Q8G_EINVAL, "execute_gemm: null argument");
+    const cudaStream_t s = (cudaStream_t)stream;
+    const int w = pl->writer;
+    if (w != Q8G_WRITE_RAW_I32 && w != Q8G_WRITE_REQUANT_U8 && w != Q8G_WRITE_DEQUANT_F32)
+        return fail(Q8G_EINVAL, "pipeline writer does not match the output element type");
+    if (pl->sparse) {
+        if (pl->sparse->k != k || pl->sparse->n != pb->n)
+            return fail(Q8G_EINVAL, "spmdm_block: block extents out of bounds (sparse " + std::to_string(pl->sparse->k) +
+                                        " x " + std::to_string(pl->sparse->n) + ", GEMM K " + std::to_string(k) +
+                                        ", N " + std::to_string(pb->n) + ")");
+        if (pl->sparse->device != pb->device)
+            return fail(Q8G_EINVAL, "SpMDMAdd: sparse matrix lives on another device");
+    }
+    if (w == Q8G_WRITE_REQUANT_U8 && pl->bias_add_dev)
+        return fail(Q8G_EINVAL, "Requantize writer: BiasAdd is folded into the epilogue (q8g_epilogue_create)");
+    // the hot paths when there is nothing to add
+    if (!pl->sparse && w == Q8G_WRITE_RAW_I32)
+        return gemm_common(a_dev, m, k, lda, pb, nullptr, pl->bias_add_dev, c_dev, ldc, row_begin, row_end, cache,
+                           s, true);
+    if (!pl->sparse && w == Q8G_WRITE_REQUANT_U8)
+        return gemm_common(a_dev, m, k, lda, pb, pl->ep, nullptr, c_dev, ldc, row_begin, row_end, cache, s, false);
+    if (w == Q8G_WRITE_REQUANT_U8) {
+        if (!pl->ep) return fail(Q8G_EINVAL, "pipeline writer does not match the output element type");
+        if (pl->ep->n != pb->n || pl->ep->device != pb->device)
+            return fail(Q8G_EINVAL, "execute_gemm: epilogue was built for another packed weight");
+    }
+    if (!a_dev || !c_dev || m < 1 || lda < k || ldc < pb->n) return fail(Q8G_EINVAL, "execute_gemm: output must be M x N");
+    if (row_begin < 0 || row_end > m || row_begin > row_end)
+        return fail(Q8G_EINVAL, "execute_gemm: row stripe out of range");
+    const int rows = row_end - row_begin;
+    if (rows == 0) return Q8G_OK;
+    DeviceGuard dg(pb->device);
+    const uint8_t* a0 = a_dev + (size_t)row_begin * lda;
+    cudaError_t e;
+    if (w == Q8G_WRITE_RAW_I32) {
+        // dense raw GEMM (+ BiasAdd) straight into the int32 output, outliers added in place
+        int rc = gemm_common(a_dev, m, k, lda, pb, nullptr, pl->bias_add_dev, c_dev, ldc, row_begin, row_end, cache,
+                             s, true);
+        if (rc) return rc;
+        int32_t* c0 = static_cast<int32_t*>(c_dev) + (size_t)row_begin * ldc;
+        if ((e = launch_post(w, c0, ldc, a0, lda, rows, k, pb->n, pl->sparse, nullptr, 0.0, 0, c0, ldc, s)) !=
+            cudaSuccess)
+            return cuda_fail(e, "post launch");
+        return Q8G_OK;
+    }
+    // requant / dequant: dense raw GEMM into a stream-ordered int32 workspace
+    int32_t* ws = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(int32_t) * (size_t)rows * pb->n, s)) !=
+        cudaSuccess)
+        return cuda_fail(e, "cudaMallocAsync(pipeline workspace)");
+    int rc = gemm_common(a0, rows, k, lda, pb, nullptr, w == Q8G_WRITE_DEQUANT_F32 ? pl->bias_add_dev : nullptr, ws,
+                         pb->n, 0, rows, cache, s, true);
+    if (rc == Q8G_OK) {
+        void* out0 = w == Q8G_WRITE_DEQUANT_F32 ? (void*)(static_cast<float*>(c_dev) + (size_t)row_begin * ldc)
+                                               : (void*)(static_cast<uint8_t*>(c_dev) + (size_t)row_begin * ldc);
+        if ((e = launch_post(w, ws, pb->n, a0, lda, rows, k, pb->n, pl->sparse,
+                             w == Q8G_WRITE_REQUANT_U8 ? pl->ep : nullptr, pl->dq_scale, pl->dq_zero_point, out0, ldc,
+                             s)) != cudaSuccess)
+            rc = cuda_fail(e, "post launch");
+    }
+    cudaFreeAsync(ws, s);
+    return rc;
+}
+
+int q8g_gemm_u8s8_pipeline_host(const uint8_t* a_host, int m, int k, int lda, const q8g_packed_b* pb,
+                                const q8g_pipeline_args* pl, const int32_t* bias_add_host, void* c_host, int ldc,
+                                int row_begin, int row_end, void* stream) {
+    if (!pl || !pb || !a_host || !c_host) return fail(Q8G_EINVAL, "execute_gemm: null argument");
+    if (pl->bias_add_dev) return fail(Q8G_EINVAL, "pipeline_host: pass BiasAdd as bias_add_host");
+    if (k != pb->k) return fail(Q8G_EINVAL, "execute_gemm: A columns must equal the packed weight K");
+    if (lda < k || ldc < pb->n || m < 1) return fail(Q8G_EINVAL, "execute_gemm: output must be M x N");
+    if (row_begin < 0 || row_end > m || row_begin > row_end)
+        return fail(Q8G_EINVAL, "execute_gemm: row stripe out of range");
+    const int rows = row_end - row_begin;
+    if (rows == 0) return Q8G_OK;
+    const size_t esz = pl->writer == Q8G_WRITE_REQUANT_U8 ? 1 : 4;
+    DeviceGuard dg(pb->device);
+    const cudaStream_t s = (cudaStream_t)stream;
+    const int lda_d = round_up_i(k, 16), n = pb->n;
+    uint8_t* a_d = nullptr;
+    void* c_d = nullptr;
+    int32_t* b_d = nullptr;
+    cudaError_t e;
+    int rc = Q8G_OK;
+    if ((e = cudaMalloc(&a_d, (size_t)rows * lda_d)) != cudaSuccess || (e = cudaMalloc(&c_d, esz * rows * n)) != cudaSuccess ||
+        (bias_add_host && (e = cudaMalloc(&b_d, sizeof(int32_t) * n)) != cudaSuccess)) {
+        rc = cuda_fail(e, "cudaMalloc(pipeline staging)");
+    } else if ((e = cudaMemcpy2DAsync(a_d, lda_d, a_host + (size_t)row_begin * lda, lda, k, rows,
+                                      cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+               (bias_add_host &&
+                (e = cudaMemcpyAsync(b_d, bias_add_host, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s)) !=
+                    cudaSuccess)) {
+        rc = cuda_fail(e, "pipeline staging copy");
+    } else {
+        q8g_pipeline_args p2 = *pl;
+        p2.bias_add_dev = b_d;
+        rc = q8g_gemm_u8s8_pipeline(a_d, rows, k, lda_d, pb, &p2, c_d, n, 0, rows, nullptr, stream);
+        if (rc == Q8G_OK &&
+            ((e = cudaMemcpy2DAsync(static_cast<uint8_t*>(c_host) + esz * (size_t)row_begin * ldc, esz * ldc, c_d,
+                                    esz * n, esz * n, rows, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+             (e = cudaStreamSynchronize(s)) != cudaSuccess))
+            rc = cuda_fail(e, "pipeline result copy");
+    }
+    cudaStreamSynchronize(s);
+    if (a_d) cudaFree(a_d);
+    if (c_d) cudaFree(c_d);
+    if (b_d) cudaFree(b_d);
+    return rc;
+}
+
 }  // extern "C"
 
 template <typename OutT>

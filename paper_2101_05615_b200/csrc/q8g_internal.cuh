@@ -47,7 +47,8 @@ enum KernelFamily : int {
     kFamConvTc = 5,
     kFamDw = 6,
     kFamDwTc = 7,
-    kFamCount = 8
+    kFamPost = 8,  // general-pipeline post kernel (post.cu)
+    kFamCount = 9
 };
 void count_launch(int family);
 
@@ -111,6 +112,15 @@ struct q8g_epilogue {
     // kernels may use the magic-add / saturating-pack requant (exact then)
     bool fast_f32 = false;
     q8g::EpiRecord* rec = nullptr;  // device, np records
+};
+
+// SparseWeightCSC (sparse.hpp:13-21) on the device
+struct q8g_sparse_csc {
+    int device = 0;
+    int k = 0, n = 0, nnz = 0;
+    int32_t* col_ptr = nullptr;  // n + 1
+    int32_t* row_idx = nullptr;  // nnz
+    int8_t* values = nullptr;    // nnz
 };
 
 struct q8g_dw_filter {
@@ -181,6 +191,9 @@ bool tc_supported(const GemmArgs& g);
 bool splitk_supported(const GemmArgs& g);
 cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s);
 bool tc2_supported(const GemmArgs& g);
+cudaError_t launch_post(int writer, const int32_t* acc, int ldacc, const uint8_t* a, int lda, int rows, int k, int n,
+                        const q8g_sparse_csc* sp, const q8g_epilogue* ep, double dq_scale, int32_t dq_zp, void* out,
+                        int ldc, cudaStream_t s);
 cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s);
 int tc_trace_copy(unsigned long long* out, int max_ctas);
 

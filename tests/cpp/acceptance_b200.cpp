@@ -115,7 +115,30 @@ bool host_checks(std::string& d) {
     int b = 0, e = 0;
     q8g_partition_stripes(10, 3, 4, &b, &e);
     if (b != 8 || e != 10) return d = "partition_stripes", false;
-    d = "blocking / pipeline validation / stripes match the reference rules";
+    if (!throws_invalid([] { OutputPipeline p({SpMDMAdd{nullptr}, WriteRawI32{}}); }, "SpMDMAdd requires a sparse matrix"))
+        return d = "SpMDMAdd rule", false;
+    if (OutputPipeline({WriteDequantF32{}}).writer() != WriterKind::kDequantF32) return d = "dequant writer", false;
+    // split_outliers (sparse.hpp:33-58): dense_small + CSC rebuilds B, outliers at full value
+    Rng rng(303);
+    const auto bm = rng.i8(37, 29);
+    const SplitWeight sw = split_outliers(cview(bm), 90);
+    Matrix<int32_t> re(37, 29, 0);
+    for (int kk = 0; kk < 37; ++kk)
+        for (int j = 0; j < 29; ++j) {
+            const int v = sw.dense_small(kk, j);
+            if (std::abs(v) >= 90) return d = "dense part holds an outlier", false;
+            re(kk, j) = v;
+        }
+    for (int j = 0; j < 29; ++j)
+        for (int32_t i = sw.sparse.col_ptr[j]; i < sw.sparse.col_ptr[j + 1]; ++i) {
+            if (std::abs((int)sw.sparse.values[i]) < 90) return d = "CSC holds a small value", false;
+            re(sw.sparse.row_idx[i], j) += sw.sparse.values[i];
+        }
+    for (int kk = 0; kk < 37; ++kk)
+        for (int j = 0; j < 29; ++j)
+            if (re(kk, j) != bm(kk, j)) return d = "split_outliers does not rebuild B", false;
+    if (!throws_invalid([&] { split_outliers(cview(bm), 0); }, "threshold must be >= 1")) return d = "threshold rule", false;
+    d = "blocking / pipeline validation / stripes / split_outliers match the reference rules";
     return true;
 }
 
@@ -231,6 +254,50 @@ bool criterion6(std::string& d) {
     return true;
 }
 
+// ---- criterion 3: outlier split + SpMDMAdd reproduce the unsplit GEMM; WriteDequantF32 ----
+bool criterion3(std::string& d) {
+    Rng rng(3003);
+    for (int t = 0; t < 8; ++t) {
+        const int m = rng.integer(1, 300), n = rng.integer(1, 200), k = rng.integer(1, 400);
+        const auto a = rng.u8(m, k);
+        const auto b = rng.i8(k, n);
+        const SplitWeight sw = split_outliers(cview(b), 40 + 11 * t);
+        const PackedWeight pw = prepack_weights(cview(sw.dense_small), BlockingParams::defaults());
+        const auto exp = oracle_gemm(a, b);
+        Matrix<int32_t> out(m, n, -1);
+        run_workers(1 + t % 3, cview(a), pw, view(out), OutputPipeline({SpMDMAdd{&sw.sparse}, WriteRawI32{}}));
+        if (!(out == exp)) return d = "SpMDMAdd raw != A x B at t=" + std::to_string(t), false;
+        std::vector<int32_t> bias(n);
+        for (int j = 0; j < n; ++j) bias[j] = 7 * j - 300;
+        const QuantParams qp{0.00321, -17};
+        Matrix<float> f(m, n, 0.f);
+        run_workers(2, cview(a), pw, view(f), OutputPipeline({SpMDMAdd{&sw.sparse}, BiasAdd{bias}, WriteDequantF32{qp}}));
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < n; ++j) {
+                const int32_t acc = (int32_t)((uint32_t)exp(i, j) + (uint32_t)bias[j]);
+                const float want = (float)(qp.scale * (double)(int32_t)((uint32_t)acc - (uint32_t)qp.zero_point));
+                if (f(i, j) != want) return d = "WriteDequantF32 mismatch at t=" + std::to_string(t), false;
+            }
+        // requantize with the original B's column offsets (Requantize::col_offsets)
+        RequantParams rp;
+        rp.multiplier = 0.0009;
+        rp.zp_a = 5;
+        rp.zp_b = 2;
+        rp.zp_c = 90;
+        rp.k_total = k;
+        std::vector<int32_t> co(n, 0);
+        for (int kk = 0; kk < k; ++kk)
+            for (int j = 0; j < n; ++j) co[j] += b(kk, j);
+        Matrix<uint8_t> q1(m, n, 0), q2(m, n, 1);
+        run_workers(1, cview(a), pw, view(q1), OutputPipeline({SpMDMAdd{&sw.sparse}, Requantize{rp, &co}}));
+        const PackedWeight full = prepack_weights(cview(b), BlockingParams::defaults());
+        run_workers(1, cview(a), full, view(q2), OutputPipeline({Requantize{rp, nullptr}}));
+        if (!(q1 == q2)) return d = "split + SpMDMAdd requant != unsplit requant", false;
+    }
+    d = "split + SpMDMAdd == unsplit GEMM (raw, requant); WriteDequantF32 exact, 8 shapes";
+    return true;
+}
+
 // ---- criterion 8: determinism across workers ----
 bool criterion8(std::string& d) {
     Rng rng(8008);
@@ -268,6 +335,7 @@ int main(int argc, char** argv) {
     if (mode == "gpu") {
         run(1, criterion1);
         run(2, criterion_c0);
+        run(3, criterion3);
         run(5, criterion5);
         run(6, criterion6);
         run(8, criterion8);

@@ -2,7 +2,8 @@
 reference (oracle/_ref/libq8ref.so, built by oracle/Makefile from
 /root/reference/proj/include).  Run here, where the reference exists:
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py                  # everything
+    python tests/golden/make_golden.py --only-sparse    # 5. outlier split / SpMDMAdd / dequant
 
 Inputs are regenerable from the seeds with std::mt19937_64 (the reference
 fixture generator, restated in oracle.c and pinned by its published KAT), so
@@ -94,5 +95,49 @@ def main():
     print("golden fixtures written to", OUT)
 
 
+def main_sparse():
+    """5. outlier split + SpMDMAdd + BiasAdd with each writer (sparse.hpp:33-80,
+    pipeline.hpp:157-207): the reference splits B, then runs execute_gemm on
+    the dense part with [SpMDMAdd, BiasAdd] and WriteRawI32 / [ReluQuantized]
+    Requantize (col_offsets of the original B) / WriteDequantF32."""
+    build()
+    orc, ref = Oracle(), RefLib()
+    rng = orc.rng(4242)
+    flat, count = {}, 0
+    for t in range(12):
+        m, n, k = rng.int(1, 100), rng.int(1, 64), rng.int(1, 200)
+        a, b = rng.u8_matrix(m, k), rng.i8_matrix(k, n)
+        threshold = [16, 48, 100, 128][t % 4]
+        dense, cp, ri, vals = ref.split_outliers(b, threshold)
+        pk = ref.prepack(dense, ref.select_blocking(m, n, k))
+        bias_add = rng.ints(-5000, 5000, n) if t % 3 else None
+        mult, zp_a, zp_b, zp_c = rng.real(0.0001, 0.005), rng.int(0, 255), rng.int(-20, 20), rng.int(0, 255)
+        rq_bias = rng.ints(-1000, 1000, n)
+        relu = bool(t % 2)
+        dq_scale, dq_zp = rng.real(0.0001, 0.1), rng.int(-500, 500)
+        sp = (cp, ri, vals)
+        case = dict(m=m, n=n, k=k, a=a, b=b, threshold=threshold, col_ptr=cp, row_idx=ri, values=vals,
+                    mult=mult, zp_a=zp_a, zp_b=zp_b, zp_c=zp_c, rq_bias=rq_bias, relu=relu, dq_scale=dq_scale,
+                    dq_zp=dq_zp, col_offsets=orc.col_offsets(b),
+                    raw=pk.gemm_pipeline(a, "raw", sparse=sp, bias_add=bias_add, threads=1 + t % 3),
+                    requant=pk.gemm_pipeline(a, "requant", sparse=sp, bias_add=bias_add, mult=mult, zp_a=zp_a,
+                                             zp_b=zp_b, zp_c=zp_c, rq_bias=rq_bias, relu=relu,
+                                             col_offsets=orc.col_offsets(b), threads=1 + t % 2),
+                    dequant=pk.gemm_pipeline(a, "dequant", sparse=sp, bias_add=bias_add, dq_scale=dq_scale,
+                                             dq_zero_point=dq_zp, threads=2),
+                    dequant_dense=pk.gemm_pipeline(a, "dequant", dq_scale=dq_scale, dq_zero_point=dq_zp))
+        if bias_add is not None:
+            case["bias_add"] = bias_add
+        for key, v in case.items():
+            flat[f"{t}_{key}"] = np.asarray(v)
+        count += 1
+    np.savez_compressed(OUT / "ref_sparse.npz", count=count, **flat)
+    print("sparse / dequant fixtures written to", OUT)
+
+
 if __name__ == "__main__":
-    main()
+    if "--only-sparse" in sys.argv:
+        main_sparse()
+    else:
+        main()
+        main_sparse()

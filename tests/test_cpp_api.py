@@ -29,4 +29,4 @@ def test_cpp_acceptance_on_gpu(runner, cuda):
     r = subprocess.run([str(runner), "gpu"], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("[PASS]") == 6
+    assert r.stdout.count("[PASS]") == 7  # 0 host + 1, 2, 3 (outliers), 5, 6, 8
