@@ -101,6 +101,7 @@ _SIGS = [
     ("q8g_sparse_csc_create", _I, [_P, _P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
     ("q8g_sparse_csc_free", _I, [_P]),
     ("q8g_gemm_u8s8_pipeline", _I, [_P, _I, _I, _I, _P, C.POINTER(PipelineArgsC), _P, _I, _I, _I, _P, _P]),
+    ("q8g_gemm_u8s8_pipeline_host", _I, [_P, _I, _I, _I, _P, C.POINTER(PipelineArgsC), _P, _P, _I, _I, _I, _P]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]
