@@ -424,7 +424,7 @@ int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, in
 static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed_b* pb,
                        const q8g_epilogue* ep, const int32_t* bias_add, void* c, int ldc,
                        int row_begin, int row_end, q8g_kernel_cache* cache, cudaStream_t s,
-                       bool raw) {
+                       bool raw, const uint32_t* a_ready = nullptr, uint32_t a_epoch = 0) {
     if (!pb) return fail(Q8G_EINVAL, "execute_gemm: null packed weight");
     if (k != pb->k) return fail(Q8G_EINVAL, "execute_gemm: A columns must equal the packed weight K");
     if (m < 1 || lda < k || ldc < pb->n || !a || !c)
@@ -450,13 +450,17 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
     g.ldc = ldc;
     g.c = raw ? (void*)((int32_t*)c + (size_t)row_begin * ldc)
               : (void*)((uint8_t*)c + (size_t)row_begin * ldc);
+    g.a_ready = a_ready;
+    g.a_epoch = a_epoch;
     const int kind = resolve_tile(cache ? cache : &process_cache(), g.rows, pb->n, k,
                                   a_is_tma_aligned(g.a, lda));
     cudaError_t e;
-    if (kind != kGeneric && tc_supported(g))
+    if (kind != kGeneric && tc_supported(g)) {
         e = launch_gemm_tc(g, kind, s);
-    else
-        e = launch_gemm_simt(g, s);
+    } else {
+        e = a_ready ? stream_wait_u32(s, a_ready, a_epoch) : cudaSuccess;
+        if (e == cudaSuccess) e = launch_gemm_simt(g, s);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
     return Q8G_OK;
 }
@@ -681,12 +685,19 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
     DeviceGuard dg(pb->device);
     const int lda_d = round_up_i(k, 16), ldc_d = pb->n;
     // grow-only per-device staging buffers; host-view calls are synchronous
-    // and serialised per device by this lock
+    // and serialised per device by this lock.  A is copied on a separate
+    // stream that ends with a stream write of the call's epoch to `flag`: the
+    // GEMM is launched at the same time and streams the (immutable) weights
+    // while A is in flight (the split-K kernel polls the flag before its first
+    // A load; other kernels wait on it in-stream).
     struct Staging {
         std::mutex mu;
         void* a = nullptr;
         void* c = nullptr;
         size_t a_bytes = 0, c_bytes = 0;
+        cudaStream_t copy = nullptr;
+        uint32_t* flag = nullptr;
+        uint32_t epoch = 0;
     };
     static Staging staging[64];
     Staging& st = staging[pb->device & 63];
@@ -707,20 +718,31 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
         if ((e = cudaMalloc(&st.c, need_c)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(C staging)");
         st.c_bytes = need_c;
     }
+    if (!st.copy) {
+        if ((e = cudaStreamCreateWithFlags(&st.copy, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "copy stream");
+        if ((e = cudaMalloc(&st.flag, sizeof(uint32_t))) != cudaSuccess ||
+            (e = cudaMemsetAsync(st.flag, 0, sizeof(uint32_t), st.copy)) != cudaSuccess)
+            return cuda_fail(e, "A-ready flag");
+    }
+    uint32_t epoch = ++st.epoch;
+    if (epoch == 0) epoch = ++st.epoch;
     uint8_t* d_a = (uint8_t*)st.a;
     OutT* d_c = (OutT*)st.c;
     int rc = Q8G_OK;
     e = cudaMemcpy2DAsync(d_a, lda_d, a_host + (size_t)row_begin * lda, lda, k, rows,
-                          cudaMemcpyHostToDevice, s);
+                          cudaMemcpyHostToDevice, st.copy);
+    if (e == cudaSuccess) e = stream_write_u32(st.copy, st.flag, epoch);
     if (e != cudaSuccess) rc = cuda_fail(e, "H2D A");
     if (!rc) {
         if (raw)
-            rc = q8g_gemm_u8s8_raw_i32(d_a, rows, k, lda_d, pb, nullptr, (int32_t*)d_c, ldc_d, 0,
-                                       rows, nullptr, s);
+            rc = gemm_common(d_a, rows, k, lda_d, pb, nullptr, nullptr, d_c, ldc_d, 0, rows, nullptr, s, true,
+                             st.flag, epoch);
         else
-            rc = q8g_gemm_u8s8_requant(d_a, rows, k, lda_d, pb, ep, (uint8_t*)d_c, ldc_d, 0, rows,
-                                       nullptr, s);
+            rc = gemm_common(d_a, rows, k, lda_d, pb, ep, nullptr, d_c, ldc_d, 0, rows, nullptr, s, false,
+                             st.flag, epoch);
     }
+    if (rc) cudaStreamSynchronize(st.copy);  // never leave the copy in flight into freed staging
     if (!rc) {
         e = cudaMemcpy2DAsync(c_host + (size_t)row_begin * ldc, sizeof(OutT) * ldc, d_c,
                               sizeof(OutT) * ldc_d, sizeof(OutT) * pb->n, rows,

@@ -78,8 +78,25 @@ struct SkParams {
     // L2 exchange workspace [tile][owner][S-1 slots] of SLOT_BYTES; null =
     // push the slots into the owners' smem (DSMEM)
     uint8_t* ws;
+    // host-view overlap: A lands by a concurrent copy that then writes a_epoch
+    // to *a_ready (GemmArgs); null = A resident
+    const uint32_t* a_ready;
+    uint32_t a_epoch;
     unsigned long long* trace;  // debug stamps (Q8G_TC_TRACE), else null
 };
+
+// poll the A-ready flag (acquire), then order the TMA (async proxy) reads of A
+// after it; trap instead of hanging if the copy never lands (~8 s)
+__device__ __forceinline__ void wait_a_ready(const uint32_t* flag, uint32_t epoch) {
+    for (long long i = 0;; ++i) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v == epoch) break;
+        if (i > (1LL << 26)) __trap();
+        __nanosleep(128);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 // slots: 0 entry, 1 prologue, 2 first TMA, 3 first stage, 4 last MMA commit,
 // 5 past the exchange's cluster barrier, 6 exchange stores issued, 7 done;
@@ -202,6 +219,10 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
 
     if (warp == 0) {
         // whole warp runs the loop; one elected lane issues (ptx::elect_one)
+        if (p.a_ready) {
+            if (ptx::elect_one()) wait_a_ready(p.a_ready, p.a_epoch);
+            __syncwarp();
+        }
         int stage = 0;
         uint32_t phase = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -494,6 +515,8 @@ cudaError_t launch_sk(const GemmArgs& g, cudaStream_t s) {
     p.zp_c = g.ep ? g.ep->zp_c : 0;
     p.relu = g.ep ? g.ep->relu : 0;
     p.fast = (g.ep && g.ep->fast_f32) ? 1 : 0;
+    p.a_ready = g.a_ready;
+    p.a_epoch = g.a_epoch;
     p.bias_add = g.bias_add;
     p.c = g.c;
     p.ldc = g.ldc;

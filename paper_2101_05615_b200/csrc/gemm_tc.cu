@@ -345,6 +345,42 @@ unsigned long long* tc_trace_buffer() {
     return buf;
 }
 
+}  // namespace
+
+cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value) {
+    using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    static Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                   ? reinterpret_cast<Fn>(f)
+                   : nullptr;
+    }();
+    if (!fn) return cudaErrorNotSupported;
+    // default flags: ordered after (and making visible) the stream's prior writes
+    return fn((CUstream)s, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS
+               ? cudaSuccess
+               : cudaErrorUnknown;
+}
+
+cudaError_t stream_wait_u32(cudaStream_t s, const uint32_t* addr, uint32_t value) {
+    using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    static Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                   ? reinterpret_cast<Fn>(f)
+                   : nullptr;
+    }();
+    if (!fn) return cudaErrorNotSupported;
+    return fn((CUstream)s, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_EQ) == CUDA_SUCCESS ? cudaSuccess
+                                                                                                : cudaErrorUnknown;
+}
+
+namespace {
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -517,27 +553,26 @@ static int tc_cfg_override() {
 }
 
 cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
-    switch (tc_cfg_override()) {
+    const int ov = tc_cfg_override();  // tuning knob Q8G_TC_CFG (0 = automatic)
+    // split-K for small M (or forced); it is the only kernel that polls a
+    // host-view A-ready flag itself (it streams B meanwhile)
+    if ((ov == 6 || (ov == 0 && tile_kind == kSmallM)) && splitk_supported(g)) {
+        const cudaError_t e = launch_gemm_splitk(g, s);
+        if (e != cudaErrorNotSupported) return e;  // else: no workspace -> non-split kernel
+    }
+    if (g.a_ready) {
+        const cudaError_t e = stream_wait_u32(s, g.a_ready, g.a_epoch);
+        if (e != cudaSuccess) return e;
+    }
+    switch (ov) {
         case 1: return launch_modes<32, 8, 10>(g, s);
         case 2: return launch_modes<32, 1, 10>(g, s);
         case 3: return launch_modes<64, 4, 8>(g, s);
         case 4: return launch_modes<128, 2, 6>(g, s);
         case 5: return launch_modes<256, 1, 4>(g, s);
-        case 6:
-            if (splitk_supported(g)) {
-                const cudaError_t e = launch_gemm_splitk(g, s);
-                if (e != cudaErrorNotSupported) return e;  // else: no workspace -> non-split kernel
-            }
-            break;
         default: break;
     }
-    if (tile_kind == kSmallM) {
-        if (splitk_supported(g)) {
-            const cudaError_t e = launch_gemm_splitk(g, s);
-            if (e != cudaErrorNotSupported) return e;  // else: no workspace -> non-split kernel
-        }
-        return launch_modes<32, 1, 10>(g, s);
-    }
+    if (tile_kind == kSmallM) return launch_modes<32, 1, 10>(g, s);
     if (tc2_supported(g)) return launch_gemm_tc2(g, s);  // CTA-pair 256x256 tiles
     return launch_modes<256, 1, 4>(g, s);
 }

@@ -184,7 +184,16 @@ struct GemmArgs {
     void* c;            // points at row 0 of the stripe
     int ldc;
     bool raw;
+    // host-view overlap (gemm_host): A arrives by a concurrent copy that ends
+    // with a stream write of a_epoch to *a_ready.  The split-K kernel streams
+    // B first and polls the flag before its first A load; every other path
+    // makes the stream wait on the flag before launching.  null = A resident.
+    const uint32_t* a_ready = nullptr;
+    uint32_t a_epoch = 0;
 };
+// stream memory operations (driver API via cudaGetDriverEntryPoint)
+cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value);
+cudaError_t stream_wait_u32(cudaStream_t s, const uint32_t* addr, uint32_t value);  // until *addr == value
 cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s);
 bool tc_supported(const GemmArgs& g);
