@@ -98,9 +98,14 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int STAGES, int MODE, bool RS>
+// CL = CTAs per cluster: 2 (one pair) or 4 (two pairs on the same N tile and
+// adjacent M tiles: each half of B is loaded once, half by each pair, and
+// multicast to both -- 25% less L2 -> SM traffic)
+template <int STAGES, int MODE, bool RS, int CL>
 __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const Tc2Params p) {
+    static_assert(CL == 2 || CL == 4, "one or two CTA pairs per cluster");
+    constexpr int PPC = CL / 2;  // pairs per cluster
     using Cfg = Tc2Cfg<STAGES>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -110,7 +115,10 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) t2_stamp(p, 0);
     const uint32_t rank = ptx::cluster_ctarank();
-    const bool leader = rank == 0;
+    const uint32_t lrank = rank & ~1u;         // this CTA's pair leader
+    const bool leader = (rank & 1u) == 0;
+    const int q = (int)(rank >> 1);             // pair within the cluster
+    const uint16_t pair_mask = (uint16_t)(3u << lrank);
 
     const uint32_t sA = base + Cfg::A_OFF, sB = base + Cfg::B_OFF;
     const uint32_t bar0 = base + Cfg::BAR_OFF;
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full_bar(s), 1);
             ptx::mbar_init(pfull_bar(s), 1);    // leader: the follower's relay
-            ptx::mbar_init(empty_bar(s), 1);    // one multicast commit
+            ptx::mbar_init(empty_bar(s), PPC);  // one multicast commit per pair leader (B is shared)
             ptx::mbar_init(rsdone_bar(s), 8);   // leader: 4 local + 4 follower row-sum warps
         }
         for (int a = 0; a < 2; ++a) {
@@ -144,33 +152,45 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     if (warp == 2) ptx::tmem_alloc_pair<512>(ptx::smem_u32(tmem_ptr));
     ptx::tc_fence_before();
     __syncthreads();
-    cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
+    cluster_sync_all();  // every CTA's barriers exist before any remote arrive / multicast
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
     ptx::griddep_wait();  // PDL: the prologue above overlapped the previous grid
     if (threadIdx.x == 0) t2_stamp(p, 1);
 
-    const int num_pairs = gridDim.x / 2;
-    const int pair = blockIdx.x / 2;
-    const int total = p.num_m_tiles * p.num_n_tiles;
+    // cluster-level tiles: PPC adjacent 256-row M tiles x one 256-column N tile;
+    // pair q takes M tile PPC*(T / nt) + q (past the end -> zero A, no stores)
+    const int num_groups = gridDim.x / CL;
+    const int group = blockIdx.x / CL;
+    const int total = ((p.num_m_tiles + PPC - 1) / PPC) * p.num_n_tiles;
+    auto tile_m0 = [&](int T) { return (PPC * (T / p.num_n_tiles) + q) * 2 * BM + (int)(rank & 1u) * BM; };
+    auto tile_n0 = [&](int T) { return (T % p.num_n_tiles) * PN; };
 
     if (warp == 0) {
         // ------------------------------------------------ producer (both CTAs)
         const uint64_t pol_b = ptx::policy_evict_last();  // B is re-read by every M tile
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = pair; t < total; t += num_pairs) {
-            const int m0 = (t / p.num_n_tiles) * 2 * BM + (int)rank * BM;
-            const int nb = (t % p.num_n_tiles) * PN + (int)rank * HN;
+        for (int t = group; t < total; t += num_groups) {
+            const int m0 = tile_m0(t);
+            const int nb = tile_n0(t) + (int)(rank & 1u) * HN;  // this CTA's half of the pair's 256 columns
             for (int kb = 0; kb < p.nkb; ++kb) {
                 ptx::mbar_wait(empty_bar(stage), phase ^ 1);
                 if (ptx::elect_one()) {
                     ptx::mbar_arrive_expect_tx(full_bar(stage), STAGE_A + STAGE_B);
                     ptx::tma_load_2d(sA + stage * STAGE_A, &tmap_a, kb * kKBlock, m0, full_bar(stage));
-                    ptx::bulk_load_hint(sB + stage * STAGE_B, p.pb + ((size_t)kb * p.np + nb) * kKBlock, STAGE_B,
-                                        full_bar(stage), pol_b);
-                    if (kb == 0 && t == pair) t2_stamp(p, 2);
-                    if (t == pair) t2_kb(p, leader ? 0 : 4, kb);
+                    if (CL == 2) {
+                        ptx::bulk_load_hint(sB + stage * STAGE_B, p.pb + ((size_t)kb * p.np + nb) * kKBlock, STAGE_B,
+                                            full_bar(stage), pol_b);
+                    } else {
+                        // rows [64q, 64q+64) of this B half, to me and my counterpart in the other pair
+                        constexpr int PIECE = STAGE_B / 2;
+                        ptx::bulk_load_mc_hint(sB + stage * STAGE_B + q * PIECE,
+                                               p.pb + ((size_t)kb * p.np + nb + q * (HN / 2)) * kKBlock, PIECE,
+                                               full_bar(stage), (uint16_t)((1u << rank) | (1u << (rank ^ 2u))), pol_b);
+                    }
+                    if (kb == 0 && t == group) t2_stamp(p, 2);
+                    if (t == group) t2_kb(p, leader ? 0 : 4, kb);
                 }
                 __syncwarp();
                 if (++stage == STAGES) {
@@ -186,29 +206,30 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = pair; t < total; t += num_pairs) {
+        for (int t = group; t < total; t += num_groups) {
             ptx::mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + (uint32_t)(acc * PN);
             for (int kb = 0; kb < p.nkb; ++kb) {
                 ptx::mbar_wait(full_bar(stage), phase);
-                if (t == pair && lane == 0) t2_kb(p, 1, kb);
+                if (t == group && lane == 0) t2_kb(p, 1, kb);
                 ptx::mbar_wait_cluster(pfull_bar(stage), phase);
-                if (t == pair && lane == 0) t2_kb(p, 2, kb);
+                if (t == group && lane == 0) t2_kb(p, 2, kb);
                 ptx::tc_fence_after();
                 const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * STAGE_A);
                 const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * STAGE_B);
                 if (ptx::elect_one()) {
-                    if (kb == 0 && t == pair) t2_stamp(p, 3);
+                    if (kb == 0 && t == group) t2_stamp(p, 3);
 #pragma unroll
                     for (int ks = 0; ks < kKBlock / 32; ++ks)
                         ptx::mma_i8_pair(d, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb | ks) != 0);
-                    if (t == pair) t2_kb(p, 3, kb);
+                    if (t == group) t2_kb(p, 3, kb);
                 }
                 __syncwarp();
                 // both CTAs' row-sum warps have read the stage
                 if (RS) ptx::mbar_wait_cluster(rsdone_bar(stage), phase);
-                if (ptx::elect_one()) ptx::tc_commit_pair_mc(empty_bar(stage), 0x3);
+                // frees the stage in every CTA that wrote part of it (all of the cluster when B is shared)
+                if (ptx::elect_one()) ptx::tc_commit_pair_mc(empty_bar(stage), CL == 2 ? pair_mask : (uint16_t)0xF);
                 __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
@@ -216,7 +237,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 }
             }
             if (ptx::elect_one()) {
-                ptx::tc_commit_pair_mc(tfull_bar(acc), 0x3);
+                ptx::tc_commit_pair_mc(tfull_bar(acc), pair_mask);
                 t2_stamp(p, 4);
             }
             __syncwarp();
@@ -228,17 +249,17 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ follower: relay
         // "my A / B halves of this stage have landed" to the leader
-        const uint32_t peer_pfull0 = ptx::mapa_shared(pfull_bar(0), 0);
+        const uint32_t peer_pfull0 = ptx::mapa_shared(pfull_bar(0), lrank);
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = pair; t < total; t += num_pairs) {
+        for (int t = group; t < total; t += num_groups) {
             for (int kb = 0; kb < p.nkb; ++kb) {
                 ptx::mbar_wait_spin(full_bar(stage), phase);
                 if (ptx::elect_one())
                     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
                                      peer_pfull0 + 8u * stage)
                                  : "memory");
-                if (t == pair && lane == 0) t2_kb(p, 5, kb);
+                if (t == group && lane == 0) t2_kb(p, 5, kb);
                 __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
@@ -250,15 +271,15 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         // ------------------------------------------------ epilogue (both CTAs)
         const int ew = warp - 4;
         const int r = ew * 32 + lane;
-        const uint32_t leader_tempty0 = ptx::mapa_shared(tempty_bar(0), 0);
+        const uint32_t leader_tempty0 = ptx::mapa_shared(tempty_bar(0), lrank);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = pair; t < total; t += num_pairs) {
-            const int row = (t / p.num_n_tiles) * 2 * BM + (int)rank * BM + r;
-            const int n0 = (t % p.num_n_tiles) * PN;
+        for (int t = group; t < total; t += num_groups) {
+            const int row = tile_m0(t) + r;
+            const int n0 = tile_n0(t);
             ptx::mbar_wait(tfull_bar(acc), acc_phase);
             ptx::tc_fence_after();
-            if (warp == 4 && lane == 0 && t == pair) t2_stamp(p, 5);
+            if (warp == 4 && lane == 0 && t == group) t2_stamp(p, 5);
             int32_t rowsum = 0;
             if (RS) {
                 ptx::mbar_wait(rfull_bar(acc), acc_phase);
@@ -290,12 +311,12 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     } else if (RS && warp >= 8) {
         // ------------------------------------------------ row sums (both CTAs)
         const int r = (warp - 8) * 32 + lane;
-        const uint32_t leader_rsdone0 = ptx::mapa_shared(rsdone_bar(0), 0);
+        const uint32_t leader_rsdone0 = ptx::mapa_shared(rsdone_bar(0), lrank);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = pair; t < total; t += num_pairs) {
+        for (int t = group; t < total; t += num_groups) {
             ptx::mbar_wait(rempty_bar(acc), acc_phase ^ 1);
             uint32_t sum = 0;
             for (int kb = 0; kb < p.nkb; ++kb) {
@@ -340,17 +361,37 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     }
 }
 
-template <int STAGES, int MODE, bool RS>
+template <int STAGES, int MODE, bool RS, int CL>
 cudaError_t launch_tc2(const GemmArgs& g, cudaStream_t s) {
     using Cfg = Tc2Cfg<STAGES>;
-    auto kern = gemm_tc2_kernel<STAGES, MODE, RS>;
-    static bool attr_set[64] = {false};
+    auto kern = gemm_tc2_kernel<STAGES, MODE, RS, CL>;
+    static int max_clusters[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !attr_set[dev]) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(RS ? 384 : 256);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    if (dev < 64 && !max_clusters[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        attr_set[dev] = true;
+        // the persistent grid must be co-resident: as many clusters as fit at once
+        cfg.gridDim = dim3(CL * (sm_count(dev) / CL));
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = sm_count(dev) / CL;
+        }
+        max_clusters[dev] = n;
     }
     CUtensorMap tmap;
     if (!make_tmap_a_cached(&tmap, g.a, g.rows, g.k, g.lda, BM)) return cudaErrorInvalidValue;
@@ -365,22 +406,10 @@ cudaError_t launch_tc2(const GemmArgs& g, cudaStream_t s) {
     p.ea = EpiArgs{g.ep ? g.ep->rec : nullptr, g.ep ? g.ep->zp_c : 0, g.ep ? g.ep->relu : 0,
                    (g.ep && g.ep->fast_f32) ? 1 : 0, g.bias_add, g.c, g.ldc, g.pb->n};
     p.trace = tc_trace_buffer_ptr();
-    const int total = p.num_m_tiles * p.num_n_tiles;
-    const int max_pairs = sm_count(dev) / 2;
-    const int pairs = total < max_pairs ? total : max_pairs;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(RS ? 384 : 256);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
+    const int total = ((p.num_m_tiles + CL / 2 - 1) / (CL / 2)) * p.num_n_tiles;  // cluster-level tiles
+    const int maxc = dev < 64 ? max_clusters[dev] : sm_count(dev) / CL;
+    const int clusters = total < maxc ? total : maxc;
+    cfg.gridDim = dim3(CL * clusters);
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, p);
     count_launch(kFamGemmTcLargeM);
@@ -398,12 +427,26 @@ bool tc2_supported(const GemmArgs& g) {
     return !off && g.pb->np % PN == 0;
 }
 
-cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s) {
+template <int CL>
+cudaError_t launch_tc2_modes(const GemmArgs& g, cudaStream_t s) {
     constexpr int ST = 6;
-    if (g.raw) return launch_tc2<ST, 0, false>(g, s);
+    if (g.raw) return launch_tc2<ST, 0, false, CL>(g, s);
     const bool rs = g.ep->need_rowsum;
-    if (g.ep->rounding == Q8G_ROUND_F32_RNE) return rs ? launch_tc2<ST, 1, true>(g, s) : launch_tc2<ST, 1, false>(g, s);
-    return rs ? launch_tc2<ST, 2, true>(g, s) : launch_tc2<ST, 2, false>(g, s);
+    if (g.ep->rounding == Q8G_ROUND_F32_RNE)
+        return rs ? launch_tc2<ST, 1, true, CL>(g, s) : launch_tc2<ST, 1, false, CL>(g, s);
+    return rs ? launch_tc2<ST, 2, true, CL>(g, s) : launch_tc2<ST, 2, false, CL>(g, s);
+}
+
+cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s) {
+    // one pair per cluster.  Q8G_TC2_CL=4 (experiment): two pairs sharing B by
+    // multicast -- 25% less L2 traffic but measured slower at C2 (194 vs 182
+    // us: the pairs wait on each other's stage releases; L2 is not the limit)
+    static const int cl = [] {
+        const char* e = getenv("Q8G_TC2_CL");
+        return e && e[0] == '4' ? 4 : 2;
+    }();
+    if (cl == 4 && g.rows > 2 * BM) return launch_tc2_modes<4>(g, s);
+    return launch_tc2_modes<2>(g, s);
 }
 
 }  // namespace q8g

@@ -140,6 +140,15 @@ __device__ __forceinline__ void bulk_load_hint(uint32_t dst, const void* src, ui
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
 }
+// bulk copy global -> the same smem offset in every CTA of `mask`, each
+// completing tx bytes on its own barrier at the same offset
+__device__ __forceinline__ void bulk_load_mc_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                                  uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint [%0], [%1], %2, [%3], %4, %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "h"(mask), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
