@@ -50,6 +50,32 @@ def test_conv3x3_small_vs_oracle(cuda, orc, shape):
     assert (yr.cpu().numpy().reshape(-1, oc) == acc).all()
 
 
+# conv_tc extremes: C in {32, 64, 128}, OC up to 240 (two 256-column TMEM
+# accumulators), the widest W (2 rows x (W+2) <= 128), odd H; ReLU on / off and
+# zp_c at both ends of the saturating-pack fast path.  The CUDA-core kernel
+# runs when the tile does not fit: W = 63, C = 48, or C = 128 with OC = 240
+# (operand image 294 KB > shared memory)
+@pytest.mark.parametrize("shape,relu,zp_c,fam", [((2, 5, 62, 32, 16), False, 0, "conv_tc"),
+                                                 ((1, 7, 20, 64, 240), True, 255, "conv_tc"),
+                                                 ((1, 5, 9, 128, 112), False, 3, "conv_tc"),
+                                                 ((3, 4, 11, 64, 112), False, 255, "conv_tc"),
+                                                 ((1, 2, 63, 32, 32), True, 5, "conv_simt"),
+                                                 ((1, 3, 8, 48, 32), False, 9, "conv_simt"),
+                                                 ((1, 3, 6, 128, 240), True, 5, "conv_simt")])
+def test_conv3x3_edge_shapes_vs_oracle(cuda, orc, shape, relu, zp_c, fam):
+    import dataclasses
+    nb, h, w, c, oc = shape
+    cc = dataclasses.replace(configs.conv_case(orc, nb, h, w, c, oc, seed=3 * sum(shape)), relu=relu, zp_c=zp_c)
+    pw = q8.prepack_conv3x3_weights(cc.w)
+    _, exp = conv_oracle(orc, cc)
+    before = q8.launch_stats()[fam]
+    y = torch.zeros((nb, h, w, oc), dtype=torch.uint8, device="cuda")
+    q8.execute_conv3x3(dev(cc.x), pw, y, conv_pipeline(cc, c))
+    torch.cuda.synchronize()
+    assert (y.cpu().numpy().reshape(-1, oc) == exp).all()
+    assert q8.launch_stats()[fam] == before + 1
+
+
 def test_conv3x3_c3_full_vs_oracle(cuda, orc):
     cc = configs.conv_case(orc)  # 32x56x56x64 -> 64, BASELINE configs[3]
     pw = q8.prepack_conv3x3_weights(cc.w)
@@ -82,6 +108,37 @@ def test_dwconv_small_vs_oracle(cuda, orc, shape):
     q8.execute_dwconv3x3(dev(dc.x), dw_filter(dc), y)
     torch.cuda.synchronize()
     assert (y.cpu().numpy() == exp).all()
+
+
+# dwconv_tc64 (C % 64 == 0, W + 2 <= 128): one / several channel blocks, odd H
+# (tail row block), W = 1 and the widest W; the 16-channel kernel for C % 64
+# != 0; the CUDA-core kernel when a 16-channel unit no longer fits one TMEM
+# buffer (W = 200); ReLU on and off, zp_c at both ends
+@pytest.mark.parametrize("shape,relu,zp_c,fam", [((3, 5, 7, 64), True, 5, "dw_tc"), ((1, 1, 1, 64), False, 0, "dw_tc"),
+                                                 ((2, 9, 126, 128), False, 255, "dw_tc"),
+                                                 ((1, 2, 1, 192), True, 200, "dw_tc"),
+                                                 ((2, 4, 30, 48), False, 17, "dw_tc"),
+                                                 ((1, 3, 200, 64), True, 5, "dw_simt"),
+                                                 ((4, 7, 13, 256), False, 128, "dw_tc")])
+def test_dwconv_tc_edge_shapes_vs_oracle(cuda, orc, shape, relu, zp_c, fam):
+    import dataclasses
+    nb, h, w, c = shape
+    dc = dataclasses.replace(configs.dw_case(orc, nb, h, w, c, seed=7 * sum(shape)), relu=relu, zp_c=zp_c)
+    exp, _ = orc.dwconv3x3(dc.x, dc.zp_a, dc.w, dc.zp_w, dc.bias, dc.mult_f32, dc.zp_c, dc.relu)
+    before = q8.launch_stats()[fam]
+    f = dw_filter(dc)
+    xd = dev(dc.x)
+    y = torch.zeros(shape, dtype=torch.uint8, device="cuda")
+    q8.execute_dwconv3x3(xd, f, y)
+    torch.cuda.synchronize()
+    assert (y.cpu().numpy() == exp).all()
+    assert q8.launch_stats()[fam] == before + 1  # the expected kernel family ran
+    if nb > 1:  # image shards compose
+        y2 = torch.zeros_like(y)
+        for i0, i1 in [(0, 1), (1, nb)]:
+            q8.execute_dwconv3x3(xd, f, y2, image_begin=i0, image_end=i1)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y2)
 
 
 def test_dwconv_c4_full_vs_oracle(cuda, orc):
