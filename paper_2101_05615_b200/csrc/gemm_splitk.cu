@@ -558,11 +558,21 @@ cudaError_t launch_sk_modes(const GemmArgs& g, cudaStream_t s) {
 bool splitk_supported(const GemmArgs& g) { return g.pb->kp / kKBlock >= 4; }
 
 cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s) {
-    static const int stages = [] {  // tuning knob: Q8G_SK_STAGES=5
+    static const int stages = [] {  // tuning knob: Q8G_SK_STAGES=3|4|5|6
         const char* e = getenv("Q8G_SK_STAGES");
         return e ? std::atoi(e) : 6;
     }();
-    return stages == 5 ? launch_sk_modes<128, 4, 5>(g, s) : launch_sk_modes<128, 4, 6>(g, s);
+    static const bool bn64 = [] {  // tuning knob: Q8G_SK_CFG=64x2 (BN 64, 2-way split)
+        const char* e = getenv("Q8G_SK_CFG");
+        return e && std::strcmp(e, "64x2") == 0;
+    }();
+    if (bn64) return launch_sk_modes<64, 2, 6>(g, s);
+    switch (stages) {
+        case 3: return launch_sk_modes<128, 4, 3>(g, s);
+        case 4: return launch_sk_modes<128, 4, 4>(g, s);
+        case 5: return launch_sk_modes<128, 4, 5>(g, s);
+        default: return launch_sk_modes<128, 4, 6>(g, s);
+    }
 }
 
 }  // namespace q8g
