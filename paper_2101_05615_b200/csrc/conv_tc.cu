@@ -62,6 +62,7 @@ struct CvParams {
     int32_t zp_a, zp_c;
     int relu, rounding;
     int fast;         // F32 fast path (0 <= zp_c <= 255, epi_f32_fast)
+    int img_prefetch; // operand image built by an earlier call: load it before griddepcontrol.wait
     int debug;        // Q8G_CONV_DEBUG bits (timing experiments only): 1 skip epilogue body, 2 skip MMAs, 4 one MMA per unit, 8 no tcgen05 fence in the MMA loop
     void* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): CTA 0 per-unit stamps, else null
@@ -250,9 +251,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             ptx::mbar_init(tempty_bar(a), 4);  // the 4 warps of the unit's warpgroup
         }
         ptx::fence_mbar_init();
-        ptx::griddep_wait();  // PDL: the operand image may come from the preceding grid
-        ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
-        ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
+        // the image is immutable once an earlier call built it: fetch it while
+        // the previous grid drains (PDL); a fresh one waits for conv_prep_kernel
+        if (p.img_prefetch) {
+            ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
+            ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
+        }
         cv_pstamp(p, 0);
     }
     // halo guard bands (windows start one position early / run past the end)
@@ -271,7 +275,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
-    ptx::griddep_wait();  // PDL: inputs / outputs are touched only after the previous grid
+    // PDL: x is read (producer) and y written (epilogue) only after
+    // griddepcontrol.wait; the MMA warp touches only smem / TMEM
     if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -280,6 +285,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ halo producer
+        ptx::griddep_wait();
+        if (!p.img_prefetch && ptx::elect_one()) {  // image built by this call's conv_prep_kernel
+            ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
+            ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
+        }
+        __syncwarp();
         int b = 0;
         uint32_t ph = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -386,6 +397,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
         }
+        ptx::griddep_wait();  // y may be read / written by the previous grid
         int i = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++i) {
             if ((i & 1) != wg) continue;
@@ -562,7 +574,9 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     // per-weight operand image, built once per (weight, C) on first use (the
     // first conv call on a weight must not be inside a stream capture)
     auto* pw = const_cast<q8g_packed_b*>(a.pw);
+    p.img_prefetch = 1;
     if (pw->conv_img_c != a.c) {
+        p.img_prefetch = 0;
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(s, &cs);
         if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
-    ptx::griddep_wait();
+    // (filter tables are immutable: built before griddepcontrol.wait, PDL)
 
     // ---- block-diagonal B = [W | Z] for every channel group (built once):
     // rows 0-15 W[t][c'] on the diagonal, rows 16-31 -zp_w[c'] on the diagonal
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ halo producer
+        ptx::griddep_wait();  // x may be the previous grid's output
         // (whole warp runs the loop; one elected lane issues)
         {
             int b = 0;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         // (TMEM allocator; idle during the main loop)
     } else if (warp >= 4) {
         // ------------------------------------------------ requant epilogue
+        ptx::griddep_wait();  // y may be read / written by the previous grid
         const int ew = warp - 4;          // 0..7
         const int quarter = ew % 4;       // TMEM lanes [32*quarter, +32)
         const int half = ew / 4;          // even / odd tiles
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
-    ptx::griddep_wait();
+    // (filter tables are immutable: built before griddepcontrol.wait, PDL)
 
     // ---- B for this channel block, per (tap, K-group): [K half][64 rows][16 B];
     // row n < 32: w[t][c0 + 32j + n] at K index n; row 32 + n: -zp_w at K index n
@@ -479,6 +481,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ halo producer
+        ptx::griddep_wait();  // x may be the previous grid's output
         int b = 0;
         uint32_t ph = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas) {
@@ -543,6 +546,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ requant epilogue
+        ptx::griddep_wait();  // y may be read / written by the previous grid
         // warpgroup r = output row r of the unit; thread = one position
         const int ew = warp - 4, r = ew / 4, quarter = ew % 4;
         const int m = quarter * 32 + lane, ocol = m - 1;
