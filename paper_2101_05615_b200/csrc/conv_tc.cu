@@ -63,7 +63,6 @@ struct CvParams {
     int relu, rounding;
     int fast;         // F32 fast path (0 <= zp_c <= 255, epi_f32_fast)
     int img_prefetch; // operand image built by an earlier call: load it before griddepcontrol.wait
-    int debug;        // Q8G_CONV_DEBUG bits (timing experiments only): 1 skip epilogue body, 2 skip MMAs, 4 one MMA per unit, 8 no tcgen05 fence in the MMA loop
     void* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): CTA 0 per-unit stamps, else null
 };
@@ -334,7 +333,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             if (lane == 0) cv_stamp(p, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
             ptx::mbar_wait(full_bar(b), ph);
             if (lane == 0) cv_stamp(p, 6, (u - (int)blockIdx.x) / (int)gridDim.x);
-            if (!(p.debug & 8)) ptx::tc_fence_after();
+            ptx::tc_fence_after();
             // start-address field (16-byte units) of halo position -1
             const uint64_t halo16 = (base + L.halo_off + b * L.halo_stride - (uint32_t)p.c) >> 4;
             const uint32_t d = tmem_base + (uint32_t)(acc * p.acc_cols);
@@ -342,7 +341,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 cv_stamp(p, 1, (u - (int)blockIdx.x) / (int)gridDim.x);
 #pragma unroll
                 for (int i = 0; i < 9 * KS; ++i)
-                    if (!(p.debug & 2) && (!(p.debug & 4) || i == 0)) ptx::mma_i8(d, a_t[i] + halo16, b_t[i], idesc, i != 0);
+                    ptx::mma_i8(d, a_t[i] + halo16, b_t[i], idesc, i != 0);
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
                 cv_stamp(p, 2, (u - (int)blockIdx.x) / (int)gridDim.x);
@@ -413,7 +412,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.acc_cols);
             const size_t pix = ((size_t)n * p.h + oh) * p.w + ocol;
             int32_t rowsum = 0;
-            for (int ch0 = 0; ch0 < ((p.debug & 1) ? 0 : p.oc_pad); ch0 += 64) {
+            for (int ch0 = 0; ch0 < p.oc_pad; ch0 += 64) {
                 // up to 64 columns (+ the row-sum column) in flight, one wait
                 uint32_t v4[4][16], rs[16];
                 const int nchunk = (p.oc_pad - ch0) >= 64 ? 4 : (p.oc_pad - ch0) / 16;
@@ -532,7 +531,6 @@ CvParams make_params(const ConvArgs& a) {
     p.relu = a.raw ? 0 : a.ep->relu;
     p.rounding = a.raw ? 0 : a.ep->rounding;
     p.fast = (!a.raw && a.ep->fast_f32) ? 1 : 0;
-    p.debug = getenv("Q8G_CONV_DEBUG") ? std::atoi(getenv("Q8G_CONV_DEBUG")) : 0;
     p.y = a.y;
     p.trace = tc_trace_buffer_ptr();
     // as many halo buffers as fit next to the operand image (>= 2)
