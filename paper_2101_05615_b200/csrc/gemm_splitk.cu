@@ -44,7 +44,9 @@ namespace {
 constexpr int BM = 128;
 constexpr int A_STAGE = BM * kKBlock;
 
-template <int BN, int S, int STAGES>
+// AST A stages, BST B stages (separate rings; the first min(BST, k-blocks)
+// stages of B are requested at kernel entry, ahead of griddepcontrol.wait)
+template <int BN, int S, int AST, int BST>
 struct SkCfg {
     static constexpr int OWN = BN / S;  // columns owned per rank
     static constexpr int B_STAGE = BN * kKBlock;
@@ -52,12 +54,12 @@ struct SkCfg {
     // one exchange slot: partials [OWN/4 quads][BM rows] int4, then [BM] row sums
     static constexpr int SLOT_PART = (OWN / 4) * BM * 16;
     static constexpr int SLOT_BYTES = SLOT_PART + BM * 4;
-    static constexpr int A_OFF = 0;  // also the send staging area after the mainloop
-    static constexpr int B_OFF = STAGES * A_STAGE;
-    static constexpr int OWNRS_OFF = B_OFF + STAGES * B_STAGE;
+    static constexpr int A_OFF = 0;
+    static constexpr int B_OFF = AST * A_STAGE;
+    static constexpr int OWNRS_OFF = B_OFF + BST * B_STAGE;
     static constexpr int REC_OFF = OWNRS_OFF + BM * 4;  // [OWN] EpiRecord
     static constexpr int BAR_OFF = REC_OFF + OWN * 16;
-    static constexpr int NUM_BARS = 3 * STAGES + 2;  // full, empty, rsdone, tfull, rsready
+    static constexpr int NUM_BARS = 3 * AST + 2 * BST + 2;  // a_full, a_empty, rsdone, b_full, b_empty, tfull, rsready
     static constexpr int TMEMPTR_OFF = BAR_OFF + NUM_BARS * 8;
     static constexpr int SMEM_BYTES = TMEMPTR_OFF + 16 + 1024;
     static_assert(SLOT_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
@@ -147,10 +149,10 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
     return d;
 }
 
-template <int BN, int S, int STAGES, int MODE, bool RS>
+template <int BN, int S, int AST, int BST, int MODE, bool RS>
 __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmap_a, const SkParams p) {
-    using Cfg = SkCfg<BN, S, STAGES>;
+    using Cfg = SkCfg<BN, S, AST, BST>;
     constexpr int OWN = Cfg::OWN;
     constexpr int NH = OWN / 16;  // 16-column chunks per owned block, split over 2 epilogue groups
     static_assert(OWN % 32 == 0, "owned column block must be a multiple of 32");
@@ -173,21 +175,27 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
 
     const uint32_t sA = base + Cfg::A_OFF, sB = base + Cfg::B_OFF;
     const uint32_t bar0 = base + Cfg::BAR_OFF;
-    auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
-    auto rsdone_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
-    const uint32_t tfull = bar0 + 8u * (3 * STAGES);
-    const uint32_t rsready = bar0 + 8u * (3 * STAGES + 1);
+    auto afull_bar = [&](int s) { return bar0 + 8u * s; };
+    auto aempty_bar = [&](int s) { return bar0 + 8u * (AST + s); };
+    auto rsdone_bar = [&](int s) { return bar0 + 8u * (2 * AST + s); };
+    auto bfull_bar = [&](int s) { return bar0 + 8u * (3 * AST + s); };
+    auto bempty_bar = [&](int s) { return bar0 + 8u * (3 * AST + BST + s); };
+    const uint32_t tfull = bar0 + 8u * (3 * AST + 2 * BST);
+    const uint32_t rsready = tfull + 8u;
     int32_t* ownrs = reinterpret_cast<int32_t*>(smem + Cfg::OWNRS_OFF);
     const int4* recs = reinterpret_cast<const int4*>(smem + Cfg::REC_OFF);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + Cfg::TMEMPTR_OFF);
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
-        for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(full_bar(s), 1);
-            ptx::mbar_init(empty_bar(s), 1);
+        for (int s = 0; s < AST; ++s) {
+            ptx::mbar_init(afull_bar(s), 1);
+            ptx::mbar_init(aempty_bar(s), 1);
             ptx::mbar_init(rsdone_bar(s), 4);
+        }
+        for (int s = 0; s < BST; ++s) {
+            ptx::mbar_init(bfull_bar(s), 1);
+            ptx::mbar_init(bempty_bar(s), 1);
         }
         ptx::mbar_init(tfull, 1);
         ptx::mbar_init(rsready, 4);
@@ -202,14 +210,15 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     // previous grid.  Packed weights are immutable once q8g_pack_b* returned
     // (it synchronizes), so no kernel in flight can be writing them; A may be
     // the previous grid's output and is only loaded after griddepcontrol.wait.
-    const int npre = (kb1 - kb0) < STAGES ? (kb1 - kb0) : STAGES;
+    const int nkl = kb1 - kb0;  // this rank's k-blocks
+    const int npre = nkl < BST ? nkl : BST;
     const uint64_t pol_b = ptx::policy_evict_first();  // weights streamed once
     if (warp == 0) {
         if (ptx::elect_one()) {
             for (int i = 0; i < npre; ++i) {
-                ptx::mbar_arrive_expect_tx(full_bar(i), A_STAGE + Cfg::B_STAGE);
+                ptx::mbar_arrive_expect_tx(bfull_bar(i), Cfg::B_STAGE);
                 ptx::bulk_load_hint(sB + i * Cfg::B_STAGE, p.pb + ((size_t)(kb0 + i) * p.np + n0) * kKBlock,
-                                    Cfg::B_STAGE, full_bar(i), pol_b);
+                                    Cfg::B_STAGE, bfull_bar(i), pol_b);
             }
         }
         __syncwarp();
@@ -223,50 +232,51 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             if (ptx::elect_one()) wait_a_ready(p.a_ready, p.a_epoch);
             __syncwarp();
         }
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
-            ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+        for (int j = 0; j < nkl; ++j) {
+            const int kb = kb0 + j;
+            const int sa = j % AST, sb = j % BST;
+            ptx::mbar_wait(aempty_bar(sa), ((uint32_t)(j / AST) & 1u) ^ 1u);
             if (ptx::elect_one()) {
-                if (kb - kb0 >= npre) {  // (the first npre stages' B went out before the PDL wait)
-                    ptx::mbar_arrive_expect_tx(full_bar(stage), A_STAGE + Cfg::B_STAGE);
-                    ptx::bulk_load_hint(sB + stage * Cfg::B_STAGE, p.pb + ((size_t)kb * p.np + n0) * kKBlock,
-                                        Cfg::B_STAGE, full_bar(stage), pol_b);
-                }
-                ptx::tma_load_2d(sA + stage * A_STAGE, &tmap_a, kb * kKBlock, m0, full_bar(stage));
+                ptx::mbar_arrive_expect_tx(afull_bar(sa), A_STAGE);
+                ptx::tma_load_2d(sA + sa * A_STAGE, &tmap_a, kb * kKBlock, m0, afull_bar(sa));
                 if (kb == kb0) sk_stamp(p, 2);
-                sk_kb(p, 0, kb - kb0);
+                sk_kb(p, 0, j);
             }
             __syncwarp();
-            if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
+            if (j >= npre) {  // B slots are reused only when the slice exceeds BST k-blocks
+                ptx::mbar_wait(bempty_bar(sb), ((uint32_t)(j / BST) & 1u) ^ 1u);
+                if (ptx::elect_one()) {
+                    ptx::mbar_arrive_expect_tx(bfull_bar(sb), Cfg::B_STAGE);
+                    ptx::bulk_load_hint(sB + sb * Cfg::B_STAGE, p.pb + ((size_t)kb * p.np + n0) * kKBlock,
+                                        Cfg::B_STAGE, bfull_bar(sb), pol_b);
+                }
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t idesc = ptx::idesc_u8s8_s32<BM, BN>();
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
-            ptx::mbar_wait(full_bar(stage), phase);
+        for (int j = 0; j < nkl; ++j) {
+            const int sa = j % AST, sb = j % BST;
+            const uint32_t pa = (uint32_t)(j / AST) & 1u;
+            ptx::mbar_wait(afull_bar(sa), pa);
+            ptx::mbar_wait(bfull_bar(sb), (uint32_t)(j / BST) & 1u);
             ptx::tc_fence_after();
-            const uint64_t adesc = ptx::sw128_kmajor_desc(sA + stage * A_STAGE);
-            const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * Cfg::B_STAGE);
+            const uint64_t adesc = ptx::sw128_kmajor_desc(sA + sa * A_STAGE);
+            const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + sb * Cfg::B_STAGE);
             if (ptx::elect_one()) {
-                if (kb == kb0) sk_stamp(p, 3);
-                sk_kb(p, 1, kb - kb0);
+                if (j == 0) sk_stamp(p, 3);
+                sk_kb(p, 1, j);
 #pragma unroll
                 for (int ks = 0; ks < kKBlock / 32; ++ks)
-                    ptx::mma_i8(tmem_base, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                    ptx::mma_i8(tmem_base, adesc + 2 * ks, bdesc + 2 * ks, idesc, (j > 0 || ks > 0) ? 1u : 0u);
             }
             __syncwarp();
-            if (RS) ptx::mbar_wait(rsdone_bar(stage), phase);
-            if (ptx::elect_one()) ptx::tc_commit(empty_bar(stage));  // same lane as the MMAs
-            __syncwarp();
-            if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
+            if (RS) ptx::mbar_wait(rsdone_bar(sa), pa);
+            if (ptx::elect_one()) {  // same lane as the MMAs
+                ptx::tc_commit(aempty_bar(sa));
+                ptx::tc_commit(bempty_bar(sb));
             }
+            __syncwarp();
         }
         if (ptx::elect_one()) {
             ptx::tc_commit(tfull);
@@ -275,12 +285,11 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         __syncwarp();
     } else if (RS && warp >= 8) {
         const int r = (warp - 8) * 32 + lane;
-        int stage = 0;
-        uint32_t phase = 0;
         uint32_t sum = 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
-            ptx::mbar_wait(full_bar(stage), phase);
-            const uint8_t* rowp = smem + Cfg::A_OFF + stage * A_STAGE + r * kKBlock;
+        for (int j = 0; j < nkl; ++j) {
+            const int sa = j % AST;
+            ptx::mbar_wait(afull_bar(sa), (uint32_t)(j / AST) & 1u);
+            const uint8_t* rowp = smem + Cfg::A_OFF + sa * A_STAGE + r * kKBlock;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const uint4 w = *reinterpret_cast<const uint4*>(rowp + ((q + r) & 7) * 16);
@@ -290,11 +299,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 sum = ptx::dp4a_uu(w.w, 0x01010101u, sum);
             }
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(rsdone_bar(stage));
-            if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
-            }
+            if (lane == 0) ptx::mbar_arrive(rsdone_bar(sa));
         }
         ownrs[r] = (int32_t)sum;  // partial over this rank's K-slice
         __syncwarp();
@@ -490,10 +495,10 @@ uint8_t* splitk_workspace(int dev, cudaStream_t s, size_t bytes) {
     return buf;
 }
 
-template <int BN, int S, int STAGES, int MODE, bool RS>
+template <int BN, int S, int AST, int BST, int MODE, bool RS>
 cudaError_t launch_sk(const GemmArgs& g, cudaStream_t s) {
-    using Cfg = SkCfg<BN, S, STAGES>;
-    auto kern = gemm_splitk_kernel<BN, S, STAGES, MODE, RS>;
+    using Cfg = SkCfg<BN, S, AST, BST>;
+    auto kern = gemm_splitk_kernel<BN, S, AST, BST, MODE, RS>;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -543,13 +548,13 @@ cudaError_t launch_sk(const GemmArgs& g, cudaStream_t s) {
     return e;
 }
 
-template <int BN, int S, int STAGES>
+template <int BN, int S, int AST, int BST>
 cudaError_t launch_sk_modes(const GemmArgs& g, cudaStream_t s) {
-    if (g.raw) return launch_sk<BN, S, STAGES, 0, false>(g, s);
+    if (g.raw) return launch_sk<BN, S, AST, BST, 0, false>(g, s);
     const bool rs = g.ep->need_rowsum;
     if (g.ep->rounding == Q8G_ROUND_F32_RNE)
-        return rs ? launch_sk<BN, S, STAGES, 1, true>(g, s) : launch_sk<BN, S, STAGES, 1, false>(g, s);
-    return rs ? launch_sk<BN, S, STAGES, 2, true>(g, s) : launch_sk<BN, S, STAGES, 2, false>(g, s);
+        return rs ? launch_sk<BN, S, AST, BST, 1, true>(g, s) : launch_sk<BN, S, AST, BST, 1, false>(g, s);
+    return rs ? launch_sk<BN, S, AST, BST, 2, true>(g, s) : launch_sk<BN, S, AST, BST, 2, false>(g, s);
 }
 
 }  // namespace
@@ -558,21 +563,20 @@ cudaError_t launch_sk_modes(const GemmArgs& g, cudaStream_t s) {
 bool splitk_supported(const GemmArgs& g) { return g.pb->kp / kKBlock >= 4; }
 
 cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s) {
-    static const int stages = [] {  // tuning knob: Q8G_SK_STAGES=3|4|5|6
-        const char* e = getenv("Q8G_SK_STAGES");
-        return e ? std::atoi(e) : 6;
-    }();
-    static const bool bn64 = [] {  // tuning knob: Q8G_SK_CFG=64x2 (BN 64, 2-way split)
+    // default: BN 128, 4-way split, 6 A + 6 B stages.  Tuning knob Q8G_SK_CFG:
+    // "64x2" (BN 64, 2-way split) or "b8" (4 A + 8 B stages: a rank's whole B
+    // slice at K = 4096 requested at entry) -- both measured slower in the
+    // bench (8.66 / 8.97 vs 8.49 us: with all of B in flight each rank's first
+    // stage lands later, and the weights still stream at ~4 TB/s)
+    static const int cfg = [] {
         const char* e = getenv("Q8G_SK_CFG");
-        return e && std::strcmp(e, "64x2") == 0;
+        if (e && std::strcmp(e, "64x2") == 0) return 1;
+        if (e && std::strcmp(e, "b8") == 0) return 2;
+        return 0;
     }();
-    if (bn64) return launch_sk_modes<64, 2, 6>(g, s);
-    switch (stages) {
-        case 3: return launch_sk_modes<128, 4, 3>(g, s);
-        case 4: return launch_sk_modes<128, 4, 4>(g, s);
-        case 5: return launch_sk_modes<128, 4, 5>(g, s);
-        default: return launch_sk_modes<128, 4, 6>(g, s);
-    }
+    if (cfg == 1) return launch_sk_modes<64, 2, 4, 16>(g, s);
+    if (cfg == 2) return launch_sk_modes<128, 4, 4, 8>(g, s);
+    return launch_sk_modes<128, 4, 6, 6>(g, s);
 }
 
 }  // namespace q8g

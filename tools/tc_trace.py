@@ -27,22 +27,37 @@ def main():
     ap.add_argument("--m", type=int, default=128)
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--k", type=int, default=4096)
+    ap.add_argument("--requant", action="store_true", help="per-channel F32 requant + ReLU (the bench's pipeline)")
+    ap.add_argument("--steady", type=int, default=0,
+                    help="trace the last of this many back-to-back launches over rotating weights (> L2)")
     args = ap.parse_args()
     m, n, k = args.m, args.n, args.k
     b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device="cuda")
     a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device="cuda")
-    c = torch.empty((m, n), dtype=torch.int32, device="cuda")
     pw = q8.prepack_weights(b)
-    pipe = q8.OutputPipeline([q8.WriteRawI32()])
+    if args.requant:
+        rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=k, zp_b_per_channel=np.full(n, 3, np.int32),
+                              multiplier_f32_per_channel=np.full(n, 1e-4, np.float32), rounding=q8.ROUND_F32_RNE)
+        pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
+        c = torch.empty((m, n), dtype=torch.uint8, device="cuda")
+    else:
+        pipe = q8.OutputPipeline([q8.WriteRawI32()])
+        c = torch.empty((m, n), dtype=torch.int32, device="cuda")
     for _ in range(3):
         q8.execute_gemm(a, pw, c, pipe)
     torch.cuda.synchronize()
-    # flush L2 between the warm-up and the traced launch
-    junk = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    junk.fill_(1)
-    torch.cuda.synchronize()
-    q8.execute_gemm(a, pw, c, pipe)
-    torch.cuda.synchronize()
+    if args.steady:
+        pws = [pw] + [pw.replicate(0) for _ in range(max(1, int(2.2 * 126e6 / (k * n))))]
+        for i in range(args.steady):
+            q8.execute_gemm(a, pws[i % len(pws)], c, pipe)
+        torch.cuda.synchronize()
+    else:
+        # flush L2 between the warm-up and the traced launch
+        junk = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        junk.fill_(1)
+        torch.cuda.synchronize()
+        q8.execute_gemm(a, pw, c, pipe)
+        torch.cuda.synchronize()
     buf = (C.c_uint64 * (8 * 1024 + 2048))()
     nct = _lib.load().q8g_debug_tc_trace(buf, 2048)
     allw = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
