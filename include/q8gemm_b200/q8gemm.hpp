@@ -15,6 +15,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <map>
@@ -196,6 +197,43 @@ struct QuantParams {  // quant.hpp:18-21
     double scale = 1.0;
     int32_t zero_point = 0;
 };
+
+// quant.hpp:45-47: ties away from zero (std::llround)
+inline long long round_half_away_from_zero(double x) { return std::llround(x); }
+
+// quant.hpp:64-82: affine params covering [min(lo, 0), max(hi, 0)]
+inline QuantParams choose_quant_params(double min_val, double max_val, bool is_signed) {
+    if (!std::isfinite(min_val) || !std::isfinite(max_val))
+        throw std::invalid_argument("choose_quant_params: range bounds must be finite");
+    if (min_val > max_val) throw std::invalid_argument("choose_quant_params: min_val must be <= max_val");
+    const double lo = std::min(min_val, 0.0), hi = std::max(max_val, 0.0);
+    const int qlo = is_signed ? -128 : 0, qhi = is_signed ? 127 : 255;
+    QuantParams qp;
+    qp.scale = hi == lo ? 1.0 : (hi - lo) / (qhi - qlo);
+    qp.zero_point = static_cast<int32_t>(std::clamp<long long>(round_half_away_from_zero(qlo - lo / qp.scale), qlo, qhi));
+    return qp;
+}
+
+// quant.hpp:84-95
+template <typename Q>
+Q quantize(double x, const QuantParams& qp) {
+    static_assert(sizeof(Q) == 1, "8-bit types only");
+    const long long lo = std::is_signed<Q>::value ? -128 : 0, hi = std::is_signed<Q>::value ? 127 : 255;
+    return static_cast<Q>(std::clamp<long long>(round_half_away_from_zero(x / qp.scale) + qp.zero_point, lo, hi));
+}
+inline double dequantize(int q, const QuantParams& qp) { return qp.scale * (q - qp.zero_point); }
+
+// quant.hpp:98-110 (host; the packed weight carries its own on the device)
+inline std::vector<int32_t> compute_col_offsets(MatrixView<const int8_t> b) {
+    if (b.rows < 1 || b.cols < 1) throw std::invalid_argument("compute_col_offsets: matrix must be non-empty");
+    std::vector<int32_t> co(b.cols, 0);
+    for (int k = 0; k < b.rows; ++k)
+        for (int j = 0; j < b.cols; ++j) co[j] += b(k, j);
+    return co;
+}
+
+// kernel.hpp:34-36: largest T with 255 * (T - 1) * kcb <= 32767
+constexpr int max_i16_split_threshold(int kcb) { return 1 + 32767 / (255 * kcb); }
 
 // sparse.hpp:13-21 (host arrays; uploaded once per device on first use)
 struct SparseWeightCSC {

@@ -73,5 +73,26 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     return LIB
 
 
+CLI_SRC = PKG / "cli" / "q8gemm_cli.cpp"
+CLI = PKG / "q8gemm_b200_cli"
+
+
+def build_cli(verbose: bool = False) -> Path:
+    """The reference command-line harness (verify / bench / demo) on the C++
+    drop-in API, linked against the in-tree library."""
+    deps = [CLI_SRC, LIB, ROOT / "include" / "q8gemm_b200" / "q8gemm.hpp", ROOT / "include" / "q8g_b200.h"]
+    if CLI.exists() and CLI.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
+        return CLI
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", f"-I{ROOT / 'include'}", str(CLI_SRC), "-o", str(CLI),
+           f"-L{PKG}", "-lq8g_b200", "-Wl,-rpath,$ORIGIN", "-pthread"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stderr}")
+    return CLI
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    print(build_cli(verbose="-v" in sys.argv))

@@ -4,13 +4,18 @@
 // oracle restatement (oracle/oracle.c, itself pinned to the reference).
 //
 //   acceptance_b200 host   host-side logic only (no GPU)
-//   acceptance_b200 gpu    GPU criteria 1, 2', 5, 6, 8 + C0 REF parity
+//   acceptance_b200 gpu [CLI]  GPU criteria 1, 2', 3, 5, 6, 7, 8 + C0 REF
+//                          parity; with the CLI binary (q8gemm_b200_cli) also
+//                          criterion 7's bench leg and criterion 8's CLI runs
 //
 // Prints one line per criterion like the reference runner; exit 0 iff all pass.
 #include <cuda_runtime.h>
 
+#include <sys/wait.h>
+
 #include <chrono>
 #include <cstdio>
+#include <fstream>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -327,10 +332,87 @@ bool criterion8(std::string& d) {
     return true;
 }
 
+std::string cli_path;
+
+std::string run_capture(const std::string& cmd, int& rc) {  // stdout + stderr, exit code
+    std::string out;
+    FILE* p = popen((cmd + " 2>&1").c_str(), "r");
+    if (!p) return rc = -1, out;
+    char buf[4096];
+    size_t got;
+    while ((got = fread(buf, 1, sizeof(buf), p)) > 0) out.append(buf, got);
+    const int st = pclose(p);
+    rc = WIFEXITED(st) ? WEXITSTATUS(st) : -1;
+    return out;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---- criterion 7 (performance smoke): 512^3 through the host-view API vs the
+// single-threaded naive product, and the CLI's default bench list < 60 s ----
+bool criterion7(std::string& d) {
+    Rng rng(7007);
+    const int dim = 512;
+    const auto a = rng.u8(dim, dim);
+    const auto b = rng.i8(dim, dim);
+    auto t0 = std::chrono::steady_clock::now();
+    Matrix<int32_t> want(dim, dim, 0);
+    orc_naive_gemm_i32(a.data(), dim, dim, dim, b.data(), dim, dim, want.data(), dim, 1);
+    const double naive_s = seconds_since(t0);
+    const PackedWeight pw = prepack_weights(cview(b), BlockingParams::defaults());
+    const OutputPipeline raw({WriteRawI32{}});
+    Matrix<int32_t> out(dim, dim, 0);
+    execute_gemm(cview(a), pw, view(out), raw, KernelVariant::kAccI32, 0, 1);
+    double best = 1e30;
+    for (int r = 0; r < 3; ++r) {
+        t0 = std::chrono::steady_clock::now();
+        execute_gemm(cview(a), pw, view(out), raw, KernelVariant::kAccI32, 0, 1);
+        best = std::min(best, seconds_since(t0));
+    }
+    double bench_s = -1.0;
+    bool bench_ok = true;
+    if (!cli_path.empty()) {
+        int rc = 0;
+        t0 = std::chrono::steady_clock::now();
+        const std::string csv = run_capture(cli_path + " bench --repeats 5", rc);
+        bench_s = seconds_since(t0);
+        bench_ok = rc == 0 && bench_s < 60.0 && csv.rfind("M,N,K,variant,threads,ns_median,gops\n", 0) == 0;
+    }
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "host-view 512^3: %.4fs vs naive %.3fs (%.0fx, want >= 2x); default bench list in %.1fs (want < 60s)",
+                  best, naive_s, naive_s / best, bench_s);
+    d = buf;
+    return out == want && naive_s / best >= 2.0 && bench_ok;
+}
+
+// ---- criterion 8, CLI leg: verify / demo byte-identical across reruns, threads=4 ----
+bool criterion8_cli(std::string& d) {
+    const std::string shapes = "/tmp/q8g_b200_acceptance_shapes.txt";
+    {
+        std::ofstream f(shapes);
+        f << "# acceptance shapes\n1 1 1\n4 5 6\n1 16 16\n16 16 16\n33 7 129\n\n56 32 64\n";
+    }
+    int rc1 = 0, rc2 = 0;
+    const std::string v1 = run_capture(cli_path + " verify --shapes " + shapes + " --seed 99", rc1);
+    const std::string v2 = run_capture(cli_path + " verify --shapes " + shapes + " --seed 99", rc2);
+    if (rc1 || rc2 || v1 != v2 || v1.find("FAIL") != std::string::npos || v1.find("PASS") == std::string::npos)
+        return d = "verify runs differ or failed:\n" + v1, false;
+    const std::string demo = cli_path + " demo --m 32 --n 24 --k 48 --density 0.02 --seed 7";
+    const std::string d1 = run_capture(demo, rc1), d2 = run_capture(demo, rc2);
+    if (rc1 || rc2 || d1 != d2 || d1.find("PASS") == std::string::npos) return d = "demo runs differ or failed:\n" + d1, false;
+    const std::string v4 = run_capture(cli_path + " verify --shapes " + shapes + " --seed 99 --threads 4", rc1);
+    if (rc1 || v4.find("FAIL") != std::string::npos) return d = "threaded verify failed:\n" + v4, false;
+    d = "CLI verify and demo byte-identical across reruns; threads=4 verify passes";
+    return true;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "host";
+    if (argc > 2) cli_path = argv[2];
     run(0, host_checks);
     if (mode == "gpu") {
         run(1, criterion1);
@@ -338,7 +420,9 @@ int main(int argc, char** argv) {
         run(3, criterion3);
         run(5, criterion5);
         run(6, criterion6);
+        run(7, criterion7);
         run(8, criterion8);
+        if (!cli_path.empty()) run(8, criterion8_cli);
     }
     if (failures == 0) {
         std::printf("all gating criteria passed\n");

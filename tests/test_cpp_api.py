@@ -26,7 +26,10 @@ def test_cpp_host_logic(runner):
 
 @pytest.mark.gpu
 def test_cpp_acceptance_on_gpu(runner, cuda):
-    r = subprocess.run([str(runner), "gpu"], capture_output=True, text=True, timeout=600)
+    from paper_2101_05615_b200 import build as b
+
+    cli = b.build_cli()
+    r = subprocess.run([str(runner), "gpu", str(cli)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("[PASS]") == 7  # 0 host + 1, 2, 3 (outliers), 5, 6, 8
+    assert r.stdout.count("[PASS]") == 9  # 0 host + 1, 2, 3 (outliers), 5, 6, 7, 8, 8 (CLI leg)
