@@ -47,9 +47,19 @@ def main():
         q8.execute_gemm(a, pw, c, pipe)
     torch.cuda.synchronize()
     if args.steady:
+        # back-to-back launches over rotating weights (> L2), replayed from one
+        # CUDA graph like bench.py, so the launch spacing is the device's
         pws = [pw] + [pw.replicate(0) for _ in range(max(1, int(2.2 * 126e6 / (k * n))))]
-        for i in range(args.steady):
-            q8.execute_gemm(a, pws[i % len(pws)], c, pipe)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):  # the split-K workspace is per stream: create it before capture
+            for p_ in pws:
+                q8.execute_gemm(a, p_, c, pipe)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            for i in range(args.steady):
+                q8.execute_gemm(a, pws[i % len(pws)], c, pipe)
+        graph.replay()
         torch.cuda.synchronize()
     else:
         # flush L2 between the warm-up and the traced launch
@@ -61,6 +71,24 @@ def main():
     buf = (C.c_uint64 * (8 * 1024 + 2048))()
     nct = _lib.load().q8g_debug_tc_trace(buf, 2048)
     allw = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+    if args.steady:
+        # split-K: successive launches stamp alternate halves -> show both
+        def fresh(h):  # stamped rows of the latest launch in this half
+            h = h[h[:, 0] > 0]
+            return h[h[:, 0] > h[:, 0].max() - 50_000] if len(h) else h
+        h0, h1 = fresh(allw[:4096].reshape(512, 8)), fresh(allw[4096:8192].reshape(512, 8))
+        if len(h0) and len(h1) and abs(int(h0[:, 0].min()) - int(h1[:, 0].min())) < 100_000:
+            first, second = (h0, h1) if h0[:, 0].min() < h1[:, 0].min() else (h1, h0)
+            z = first[:, 0].min()
+            print(f"two successive launches, us from the first one's earliest entry ({len(first)} CTAs each)")
+            for nm_i, nm in enumerate(NAMES):
+                for tag, arr in (("N", first), ("N+1", second)):
+                    col = arr[:, nm_i]
+                    col = col[col > 0] - z
+                    if len(col):
+                        print(f"  {tag:3s} {nm:10s} min {col.min()/1e3:8.2f} us  med {np.median(col)/1e3:8.2f}"
+                              f"  max {col.max()/1e3:8.2f}")
+            return
     t = allw[:8 * 1024].reshape(1024, 8)[:nct]
     kbs = allw[8192:8192 + 192].reshape(3, 64)
     used = t[:, 0] > 0
