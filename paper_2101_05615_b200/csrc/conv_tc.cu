@@ -310,41 +310,43 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        // descriptor templates computed once: the issue loop is then one add
-        // + one tcgen05.mma per K-step (the warp shares its SMSP with epilogue
-        // warps, so per-MMA integer work directly slows the tensor pipe)
+        // The whole warp runs the loop (warp-uniform control flow) and one
+        // elected lane issues: every descriptor is then a uniform-register
+        // add off two bases (tap (kh, kw), K-step j: the A window starts
+        // kh rows + kw positions into the halo), so consecutive tcgen05.mma
+        // issue back to back.  (Per-lane loops over precomputed descriptor
+        // arrays compiled to R2UR moves + an ELECT loop per MMA: ~70 cycles
+        // of issue per MMA, slower than the tensor pipe.)
         const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(p.nq >> 3) << 17) | ((128u >> 4) << 24);
-        uint64_t a_t[9 * KS], b_t[9 * KS];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            const int sh1 = (t / 3) * p.wp + (t % 3);  // tap shift + 1 (non-negative)
-#pragma unroll
-            for (int j = 0; j < KS; ++j) {
-                a_t[t * KS + j] = kmajor_swz_desc((uint32_t)(sh1 * p.c + j * 32), p.c);
-                b_t[t * KS + j] = kmajor_noswz_desc(base + L.b_off + (uint32_t)(((t * KS + j) * 2) * p.nq * 16),
-                                                    (uint32_t)(p.nq * 16), 128);
-            }
-        }
+        const uint64_t row16 = (uint64_t)(p.wp * 2 * KS);  // one halo row (wp positions x C bytes) in 16-byte units
+        const uint64_t pos16 = (uint64_t)(2 * KS);         // one position
+        const uint64_t bstep = (uint64_t)(2 * p.nq);       // one (tap, K-step) block of B: 2 halves x nq rows x 16 B
+        const uint64_t b0 = kmajor_noswz_desc(base + L.b_off, (uint32_t)(p.nq * 16), 128);
+        const uint64_t a0 = kmajor_swz_desc(0u, p.c);
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         ptx::mbar_wait(img_bar, 0);
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const int ui = (u - (int)blockIdx.x) / (int)gridDim.x;
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
-            if (lane == 0) cv_stamp(p, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
+            if (lane == 0) cv_stamp(p, 5, ui);
             ptx::mbar_wait(full_bar(b), ph);
-            if (lane == 0) cv_stamp(p, 6, (u - (int)blockIdx.x) / (int)gridDim.x);
+            if (lane == 0) cv_stamp(p, 6, ui);
             ptx::tc_fence_after();
-            // start-address field (16-byte units) of halo position -1
-            const uint64_t halo16 = (base + L.halo_off + b * L.halo_stride - (uint32_t)p.c) >> 4;
+            // start-address field of halo position -1 (windows start one early)
+            const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride - (uint32_t)p.c) >> 4);
             const uint32_t d = tmem_base + (uint32_t)(acc * p.acc_cols);
             if (ptx::elect_one()) {
-                cv_stamp(p, 1, (u - (int)blockIdx.x) / (int)gridDim.x);
+                cv_stamp(p, 1, ui);
 #pragma unroll
-                for (int i = 0; i < 9 * KS; ++i)
-                    ptx::mma_i8(d, a_t[i] + halo16, b_t[i], idesc, i != 0);
+                for (int t = 0; t < 9; ++t)
+#pragma unroll
+                    for (int j = 0; j < KS; ++j)
+                        ptx::mma_i8(d, ahalo + (uint64_t)(t / 3) * row16 + (uint64_t)(t % 3) * pos16 + 2u * j,
+                                    b0 + (uint64_t)(t * KS + j) * bstep, idesc, (t | j) != 0);
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
-                cv_stamp(p, 2, (u - (int)blockIdx.x) / (int)gridDim.x);
+                cv_stamp(p, 2, ui);
             }
             __syncwarp();
             if (++b == p.nbuf) {
@@ -397,36 +399,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
         }
         ptx::griddep_wait();  // y may be read / written by the previous grid
-        int i = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++i) {
-            if ((i & 1) != wg) continue;
-            const int acc = i % p.nacc;
-            const uint32_t aph = (uint32_t)(i / p.nacc) & 1u;
-            const int n = u / p.rblocks, rb = u % p.rblocks;
-            const int oh = rb * ROWS + orow;
-            const bool valid = orow < ROWS && oh < p.h && ocol >= 0 && ocol < p.w;
-            const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
-            ptx::mbar_wait(tfull_bar(acc), aph);
-            ptx::tc_fence_after();
-            if (quarter == 0 && lane == 0) cv_stamp(p, 3, i);
-            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.acc_cols);
-            const size_t pix = ((size_t)n * p.h + oh) * p.w + ocol;
-            int32_t rowsum = 0;
-            for (int ch0 = 0; ch0 < p.oc_pad; ch0 += 64) {
-                // up to 64 columns (+ the row-sum column) in flight, one wait
-                uint32_t v4[4][16], rs[16];
-                const int nchunk = (p.oc_pad - ch0) >= 64 ? 4 : (p.oc_pad - ch0) / 16;
-                if (ch0 == 0) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)p.oc_pad, rs);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (k < nchunk) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(ch0 + 16 * k), v4[k]);
-                ptx::tmem_ld_wait();
-                if (ch0 == 0) rowsum = (int32_t)rs[0];
-                if (ch0 == 0 && quarter == 0 && lane == 0 && p.trace && blockIdx.x == 0 && i < 64) {
-                    unsigned long long tt;  // debug: TMEM loads landed
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-                    p.trace[8192 + 384 + i] = tt;
-                }
+        // requant + store of up to 64 columns (+ row sum) of one position
+        auto process = [&](const uint32_t (&v4)[4][16], int nchunk, int ch0, int32_t rowsum, int cls, bool valid,
+                           size_t pix) {
                 if (MODE == 1 && p.fast && (p.oc % 16) == 0) {
                     const int4* nzq = reinterpret_cast<const int4*>(smem + L.soa_off) + ch0 / 4;
                     const float4* mq = reinterpret_cast<const float4*>(smem + L.soa_off + p.oc_pad * 4) + ch0 / 4;
@@ -443,7 +418,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                     else
                         Q8G_EPI_FAST(false);
 #undef Q8G_EPI_FAST
-                    continue;
+                    return;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -483,6 +458,38 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                             if (ch + j < p.oc) dst[j] = (uint8_t)q[j];
                     }
                 }
+        };
+        int i = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++i) {
+            if ((i & 1) != wg) continue;
+            const int acc = i % p.nacc;
+            const uint32_t aph = (uint32_t)(i / p.nacc) & 1u;
+            const int n = u / p.rblocks, rb = u % p.rblocks;
+            const int oh = rb * ROWS + orow;
+            const bool valid = orow < ROWS && oh < p.h && ocol >= 0 && ocol < p.w;
+            const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
+            const size_t pix = ((size_t)n * p.h + oh) * p.w + ocol;
+            ptx::mbar_wait(tfull_bar(acc), aph);
+            ptx::tc_fence_after();
+            if (quarter == 0 && lane == 0) cv_stamp(p, 3, i);
+            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.acc_cols);
+            int32_t rowsum = 0;
+            for (int ch0 = 0; ch0 < p.oc_pad; ch0 += 64) {
+                // up to 64 columns (+ the row-sum column) in flight, one wait
+                uint32_t v4[4][16], rs[16];
+                const int nchunk = (p.oc_pad - ch0) >= 64 ? 4 : (p.oc_pad - ch0) / 16;
+                if (ch0 == 0) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)p.oc_pad, rs);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nchunk) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(ch0 + 16 * k), v4[k]);
+                ptx::tmem_ld_wait();
+                if (ch0 == 0) rowsum = (int32_t)rs[0];
+                if (ch0 == 0 && quarter == 0 && lane == 0 && p.trace && blockIdx.x == 0 && i < 64) {
+                    unsigned long long tt;  // debug: TMEM loads landed
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+                    p.trace[8192 + 384 + i] = tt;
+                }
+                process(v4, nchunk, ch0, rowsum, cls, valid, pix);
             }
             ptx::tc_fence_before();
             __syncwarp();

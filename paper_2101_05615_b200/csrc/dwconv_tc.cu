@@ -502,23 +502,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         constexpr uint32_t idesc = ptx::idesc_u8s8_s32<128, N2>();
-        // A templates relative to halo position -1: tile r, tap t starts at
-        // position (r + t/3)*(W+2) + t%3 - 1 (the +1 shift keeps fields >= 0)
-        uint64_t a_t[R2 * 9], b_t[9 * KG];
-#pragma unroll
-        for (int r = 0; r < R2; ++r)
-#pragma unroll
-            for (int t = 0; t < 9; ++t) a_t[r * 9 + t] = kmajor_swz64_desc((uint32_t)(((r + t / 3) * p.wp + t % 3) * CB));
-#pragma unroll
-        for (int i = 0; i < 9 * KG; ++i)
-            b_t[i] = kmajor_noswz_desc(base + L.b_off + (uint32_t)(i * 2048), 1024, 128);
+        // descriptors as uniform-register adds off two bases (an array of 36
+        // precomputed descriptors spilled out of the uniform registers and
+        // slowed the issue): tile r, tap t starts at halo position
+        // (r + t/3)*(W+2) + t%3 - 1 (the +1 shift keeps fields >= 0)
+        const uint64_t a0 = kmajor_swz64_desc(0u);
+        const uint64_t row16 = (uint64_t)(p.wp * CB / 16), pos16 = CB / 16;
+        const uint64_t b0 = kmajor_noswz_desc(base + L.b_off, 1024, 128);
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas) {
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
             ptx::mbar_wait(full_bar(b), ph);
             ptx::tc_fence_after();
-            const uint64_t halo16 = (base + L.halo_off + b * L.halo_stride - (uint32_t)CB) >> 4;
+            const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride - (uint32_t)CB) >> 4);
             if (ptx::elect_one()) {
                 dw_stamp(p, 1, (k - cta_in) / ctas);
 #pragma unroll
@@ -528,7 +525,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                         const uint32_t d = tmem_base + (uint32_t)(acc * 256 + (r * KG + j) * N2);
 #pragma unroll
                         for (int t = 0; t < 9; ++t)
-                            ptx::mma_i8(d, a_t[r * 9 + t] + halo16 + (uint64_t)(j * 2), b_t[t * KG + j], idesc, t != 0);
+                            ptx::mma_i8(d, ahalo + (uint64_t)(r + t / 3) * row16 + (uint64_t)(t % 3) * pos16 + 2u * j,
+                                        b0 + (uint64_t)((t * KG + j) * 128), idesc, t != 0);
                     }
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
