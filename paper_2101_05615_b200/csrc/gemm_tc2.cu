@@ -86,6 +86,16 @@ __device__ __forceinline__ void t2_stamp(const Tc2Params& p, int slot) {
 // first pair, first tile, per k-block (debug): [8192 + 64*which + kb]: 0 leader
 // producer issued, 1 MMA past full, 2 MMA past pfull, 3 MMAs issued, 4
 // follower producer issued, 5 follower relay sent
+// CTA 0, per tile ti < 32: [9216 + 4 * ti + k], k: 0 first MMA issued, 1 last
+// MMA issued (tfull committed), 2 epilogue start, 3 epilogue done
+// (tools/tc2_tiles.py)
+__device__ __forceinline__ void t2_tile(const Tc2Params& p, int k, int ti) {
+    if (p.trace && blockIdx.x == 0 && ti < 32) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[9216 + 4 * ti + k] = t;
+    }
+}
 __device__ __forceinline__ void t2_kb(const Tc2Params& p, int which, int kb) {
     if (p.trace && blockIdx.x < 2 && kb < 64) {
         unsigned long long t;
@@ -220,6 +230,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 const uint64_t bdesc = ptx::sw128_kmajor_desc(sB + stage * STAGE_B);
                 if (ptx::elect_one()) {
                     if (kb == 0 && t == group) t2_stamp(p, 3);
+                    if (kb == 0) t2_tile(p, 0, (t - group) / num_groups);
 #pragma unroll
                     for (int ks = 0; ks < kKBlock / 32; ++ks)
                         ptx::mma_i8_pair(d, adesc + 2 * ks, bdesc + 2 * ks, idesc, (kb | ks) != 0);
@@ -239,6 +250,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             if (ptx::elect_one()) {
                 ptx::tc_commit_pair_mc(tfull_bar(acc), pair_mask);
                 t2_stamp(p, 4);
+                t2_tile(p, 1, (t - group) / num_groups);
             }
             __syncwarp();
             if (++acc == 2) {
@@ -280,6 +292,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             ptx::mbar_wait(tfull_bar(acc), acc_phase);
             ptx::tc_fence_after();
             if (warp == 4 && lane == 0 && t == group) t2_stamp(p, 5);
+            if (warp == 4 && lane == 0) t2_tile(p, 2, (t - group) / num_groups);
             int32_t rowsum = 0;
             if (RS) {
                 ptx::mbar_wait(rfull_bar(acc), acc_phase);
@@ -303,6 +316,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                                  leader_tempty0 + 8u * acc)
                              : "memory");
             if (warp == 4 && lane == 0) t2_stamp(p, 6);
+            if (warp == 4 && lane == 0) t2_tile(p, 3, (t - group) / num_groups);
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;

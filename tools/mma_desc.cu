@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(160, 1) probe(int a_s, int a_shift, int b_swz,
                 if (readers == 4) __nanosleep(100);
                 if (readers == 7 && same_smsp) __nanosleep(100);
                 if (readers == 8 && same_smsp) __nanosleep(0);
+                if (readers == 9) __nanosleep(5000);  // ~12% duty: a 512-FMA-chain burst, then ~5 us idle
+                if (readers == 10) __nanosleep(1500);
             }
             for (int i = 0; i < 8; ++i) acc += __float_as_uint(f[i]);
         } else if (readers)
@@ -156,8 +158,8 @@ int main() {
     run(probe<80>, 80, 64, -1, 0);
     run(probe<256>, 256, 128, 0, 1);
     iters_ = 400;
-    for (readers = 2; readers <= 8; ++readers) {
-        std::printf("ALU warps, yield mode %d (0 none, 1 nanosleep(0), 2 nanosleep(100), 3 = 0, 4 no ALU warp on the MMA SMSP, 5/6 nanosleep(100)/(0) only on the MMA SMSP) every 512 FMAs\n",
+    for (readers = 2; readers <= 10; ++readers) {
+        std::printf("ALU warps, yield mode %d (0 none, 1 nanosleep(0), 2 nanosleep(100), 3 = 0, 4 no ALU warp on the MMA SMSP, 5/6 nanosleep(100)/(0) only on the MMA SMSP, 7/8 bursts then nanosleep(5000)/(1500) on all) every 512 FMAs\n",
                     readers - 2);
         run(probe<80>, 80, 64, -1, 0);
         run(probe<256>, 256, 128, 0, 1);
