@@ -346,3 +346,39 @@ def test_large_m_pair_kernel_repeated_runs_exact(cuda, orc):
     for i, o in enumerate(outs):
         assert (o.cpu().numpy() == exp).all(), i
     assert q8.launch_stats()["gemm_tc_large_m"] == before + 21
+
+
+def test_c2_full_size_row_subset_vs_oracle(cuda, orc):
+    """C2 at its full size (16384 x 4096 x 4096, the CTA-pair kernel): raw int32
+    and F32_RNE per-channel requant checked against the oracle on a row subset
+    covering tile / pair / stripe boundaries (the full naive
+    product would take minutes); two-stripe composition bit-identical."""
+    import dataclasses
+    m, n, k = configs.CONFIG_SHAPES["C2"]
+    c = configs.gemm_case(orc, "C2", m, n, k, seed=2)
+    pw = q8.prepack_weights(c.b)
+    ad = dev(c.a)
+    raw = torch.zeros((m, n), dtype=torch.int32, device="cuda")
+    q8.execute_gemm(ad, pw, raw, q8.OutputPipeline([q8.WriteRawI32()]))
+    out = torch.zeros((m, n), dtype=torch.uint8, device="cuda")
+    pipe = requant_pipeline(c, k, q8.ROUND_F32_RNE)
+    q8.execute_gemm(ad, pw, out, pipe)
+    out2 = torch.zeros((m, n), dtype=torch.uint8, device="cuda")
+    for t in (1, 0):
+        q8.execute_gemm(ad, pw, out2, pipe, thread_id=t, num_threads=2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    edges = [0, 1, 127, 128, 255, 256, 257, 8191, 8192, 8193, m - 257, m - 256, m - 129, m - 128, m - 1]
+    rows = np.array(sorted(set(edges) | set(np.random.default_rng(5).integers(0, m, 40).tolist())))
+    sub = dataclasses.replace(c, a=np.ascontiguousarray(c.a[rows]))
+    acc = orc.naive_gemm_i32(sub.a, c.b)
+    assert (raw[torch.from_numpy(rows).cuda()].cpu().numpy() == acc).all()
+    exp = oracle_requant(orc, sub, acc, 1)
+    assert (out[torch.from_numpy(rows).cuda()].cpu().numpy() == exp).all()
+    # size-independent property over all 67 M outputs: the raw accumulators'
+    # column sums equal the exact A-row-sum-weighted column sums of B
+    colsum_gpu = raw.to(torch.int64).sum(dim=0).cpu().numpy()
+    rs = c.a.astype(np.int64).sum(axis=0)  # sum over rows of A, per k
+    colsum_exact = rs @ c.b.astype(np.int64)
+    # raw int32 accumulators are exact (|acc| < 2^31 at K = 4096)
+    assert (colsum_gpu == colsum_exact).all()
