@@ -22,10 +22,14 @@ def main():
     b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device="cuda")
     a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device="cuda")
     pw = q8.prepack_weights(b)
-    rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=k, zp_b_per_channel=np.full(n, 3, np.int32),
+    zpb = 0 if "--zpb0" in sys.argv else 3  # zp_b = 0: no row sums (RS warps idle)
+    rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=k, zp_b_per_channel=np.full(n, zpb, np.int32),
                           multiplier_f32_per_channel=np.full(n, 1e-4, np.float32), rounding=q8.ROUND_F32_RNE)
     pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
     c = torch.empty((m, n), dtype=torch.uint8, device="cuda")
+    if "--raw" in sys.argv:
+        pipe = q8.OutputPipeline([q8.WriteRawI32()])
+        c = torch.empty((m, n), dtype=torch.int32, device="cuda")
     for _ in range(3):
         q8.execute_gemm(a, pw, c, pipe)
     torch.cuda.synchronize()
