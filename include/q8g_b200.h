@@ -113,7 +113,8 @@ int q8g_kernel_cache_create(int generic_only, q8g_kernel_cache** out);
 int q8g_kernel_cache_free(q8g_kernel_cache* kc);
 uint64_t q8g_kernel_cache_build_count(const q8g_kernel_cache* kc);
 /* tile kind chosen for a shape: 0 generic CUDA-core, 1 tcgen05 small-M
- * (cluster multicast), 2 tcgen05 large-M persistent */
+ * (M <= 256: split-K clusters), 2 tcgen05 large-M (persistent CTA pairs),
+ * 3 tcgen05 mid-M (M <= 1024: 128-column tiles, one wave) */
 int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, int* tile_kind);
 
 /* ---- GEMM (engine.hpp:59-169 execute_gemm) ----

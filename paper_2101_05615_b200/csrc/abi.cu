@@ -74,7 +74,9 @@ static q8g_kernel_cache& process_cache() {
 // 117-140 build).  `aligned` = TMA can address A (16B-aligned base, lda%16==0).
 static int resolve_tile(q8g_kernel_cache* kc, int rows, int n, int k, bool aligned) {
     ShapeKey key;
-    key.m_class = rows <= 128 ? 0 : 1;
+    // M classes from a sweep at N = K = 4096 (tools/tc_sweep.py): split-K wins
+    // to M = 256, 128-column tiles to ~1024, the CTA-pair kernel beyond
+    key.m_class = rows <= 256 ? 0 : rows <= 1024 ? 1 : 2;
     key.n_class = n <= 32 ? 0 : 1;
     key.k_class = k % 16 == 0 ? 0 : 1;
     key.align = aligned ? 1 : 0;
@@ -84,7 +86,7 @@ static int resolve_tile(q8g_kernel_cache* kc, int rows, int n, int k, bool align
     ++kc->builds;
     int kind = kGeneric;
     if (!kc->generic_only && key.align && key.k_class == 0)
-        kind = key.m_class == 0 ? kSmallM : kLargeM;
+        kind = key.m_class == 0 ? kSmallM : key.m_class == 1 ? kMidM : kLargeM;
     kc->table.emplace(key, kind);
     return kind;
 }

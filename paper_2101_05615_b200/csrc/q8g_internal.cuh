@@ -142,7 +142,9 @@ struct q8g_dw_filter {
 namespace q8g {
 
 // Tile kinds chosen by the dispatch cache (dispatch.hpp:248 TileKind analog)
-enum TileKind : int { kGeneric = 0, kSmallM = 1, kLargeM = 2 };
+// small M (<= 256): split-K clusters; mid M (<= 1024): 128-column 1-CTA
+// tiles in one wave; large M: persistent CTA-pair 256 x 256 tiles
+enum TileKind : int { kGeneric = 0, kSmallM = 1, kLargeM = 2, kMidM = 3 };
 
 struct ShapeKey {
     int m_class, n_class, k_class, align;

@@ -109,7 +109,7 @@ def test_kernel_cache_builds_each_class_once_under_races():
     # test_dispatch.cpp:102-129 / acceptance.cpp:389-405
     kc = q8.KernelCache()
     shapes = [(m, 64, 64, 64) for m in (1, 5, 28, 300)] + [(m, 64, 45, 45) for m in (1, 300)]
-    expected_classes = {(m <= 128, k % 16 == 0, lda % 16 == 0) for m, _, k, lda in shapes}
+    expected_classes = {(0 if m <= 256 else 1 if m <= 1024 else 2, k % 16 == 0, lda % 16 == 0) for m, _, k, lda in shapes}
 
     def race():
         for s in shapes:
@@ -122,7 +122,8 @@ def test_kernel_cache_builds_each_class_once_under_races():
         t.join()
     assert kc.build_count() == len(expected_classes)
     assert kc.tile(1, 64, 64, 64) == 1  # small-M tensor-core tile
-    assert kc.tile(300, 64, 64, 64) == 2  # large-M persistent tile
+    assert kc.tile(300, 64, 64, 64) == 3  # mid-M 128-column tiles
+    assert kc.tile(3000, 64, 64, 64) == 2  # large-M persistent CTA-pair tiles
     assert kc.tile(300, 64, 45, 45) == 0  # TMA cannot address it: generic tile
     g = q8.KernelCache(generic_only=True)
     assert g.tile(300, 64, 64, 64) == 0

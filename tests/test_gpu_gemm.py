@@ -104,15 +104,16 @@ def test_raw_random_shapes_threads(cuda, orc):
             assert (run_raw(a, pw, threads=threads) == exp).all(), (m, n, k, threads)
 
 
-@pytest.mark.parametrize("m", [1, 64, 128, 129, 200, 256, 300, 1000])
+@pytest.mark.parametrize("m", [1, 64, 128, 129, 200, 256, 257, 300, 1000, 1025, 1500])
 @pytest.mark.parametrize("n,k", [(32, 128), (256, 256), (800, 320), (300, 144), (4096, 512)])
 def test_tensor_core_paths_raw(cuda, orc, m, n, k):
     r = orc.rng(m * 7 + n * 3 + k)
     a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
     pw = q8.prepack_weights(b)
     kc = q8.KernelCache()
-    assert kc.tile(m, n, k, k) == (1 if m <= 128 else 2)
-    fam = "gemm_tc_small_m" if m <= 128 else "gemm_tc_large_m"
+    assert kc.tile(m, n, k, k) == (1 if m <= 256 else 3 if m <= 1024 else 2)
+    # launch families count tile widths: <= 128 columns (split-K, mid-M) vs 256 / pair tiles
+    fam = "gemm_tc_small_m" if m <= 1024 else "gemm_tc_large_m"
     before = q8.launch_stats()
     assert (run_raw(a, pw, cache=kc) == orc.naive_gemm_i32(a, b)).all()
     after = q8.launch_stats()
