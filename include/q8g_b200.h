@@ -112,9 +112,9 @@ int q8g_epilogue_free(q8g_epilogue* ep);
 int q8g_kernel_cache_create(int generic_only, q8g_kernel_cache** out);
 int q8g_kernel_cache_free(q8g_kernel_cache* kc);
 uint64_t q8g_kernel_cache_build_count(const q8g_kernel_cache* kc);
-/* tile kind chosen for a shape: 0 generic CUDA-core, 1 tcgen05 small-M
- * (M <= 256: split-K clusters), 2 tcgen05 large-M (persistent CTA pairs),
- * 3 tcgen05 mid-M (M <= 1024: 128-column tiles, one wave) */
+/* tile kind chosen for a shape: 0 generic CUDA-core, 1 tcgen05 split-K
+ * (when its CTAs fit two waves), 2 tcgen05 persistent CTA-pair 256 x 256 tiles
+ * (at least one tile per SM pair), 3 tcgen05 128-column tiles otherwise */
 int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, int* tile_kind);
 
 /* ---- GEMM (engine.hpp:59-169 execute_gemm) ----

@@ -72,11 +72,22 @@ static q8g_kernel_cache& process_cache() {
 
 // Shape class -> tile kind, memoized (dispatch.hpp:60-75 classify_shape,
 // 117-140 build).  `aligned` = TMA can address A (16B-aligned base, lda%16==0).
+// Tensor-core tile class by how many CTAs each kernel would fill on B200's
+// 148 SMs (from per-launch sweeps over M, N, K, tools/tc_sweep.py):
+//   0 split-K (BN 128, 4 ranks): up to two waves of its CTAs
+//   2 CTA-pair 256 x 256 tiles: at least one tile per pair of SMs
+//   1 otherwise: 128-column 1-CTA tiles (clusters of 2 sharing A rows)
+constexpr int kDispatchSms = 148;
+static int tile_class(int rows, int n) {
+    const long long mt = (rows + 127) / 128, nt = (n + 127) / 128;
+    if (mt * nt * 4 <= 2LL * kDispatchSms) return 0;
+    if ((long long)((rows + 255) / 256) * ((n + 255) / 256) >= kDispatchSms / 2) return 2;
+    return 1;
+}
+
 static int resolve_tile(q8g_kernel_cache* kc, int rows, int n, int k, bool aligned) {
     ShapeKey key;
-    // M classes from a sweep at N = K = 4096 (tools/tc_sweep.py): split-K wins
-    // to M = 256, 128-column tiles to ~1024, the CTA-pair kernel beyond
-    key.m_class = rows <= 256 ? 0 : rows <= 1024 ? 1 : 2;
+    key.m_class = tile_class(rows, n);
     key.n_class = n <= 32 ? 0 : 1;
     key.k_class = k % 16 == 0 ? 0 : 1;
     key.align = aligned ? 1 : 0;

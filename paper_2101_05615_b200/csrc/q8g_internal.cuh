@@ -142,8 +142,8 @@ struct q8g_dw_filter {
 namespace q8g {
 
 // Tile kinds chosen by the dispatch cache (dispatch.hpp:248 TileKind analog)
-// small M (<= 256): split-K clusters; mid M (<= 1024): 128-column 1-CTA
-// tiles in one wave; large M: persistent CTA-pair 256 x 256 tiles
+// small: split-K clusters; mid: 128-column 1-CTA tiles; large: persistent
+// CTA-pair 256 x 256 tiles (abi.cu tile_class)
 enum TileKind : int { kGeneric = 0, kSmallM = 1, kLargeM = 2, kMidM = 3 };
 
 struct ShapeKey {

@@ -55,6 +55,15 @@ def gemm_case(orc, name: str, m: int, n: int, k: int, seed: int = 42) -> GemmCas
     return GemmCase(name, a, b, bias, 128, zp_b, mf, 0.0, 5, True, True)
 
 
+def tile_class(m: int, n: int) -> int:
+    """abi.cu tile_class: 0 split-K within two waves of B200's 148 SMs, 2
+    CTA-pair 256 x 256 tiles when every SM pair gets one, else 1 (128-column
+    tiles)."""
+    if -(-m // 128) * -(-n // 128) * 4 <= 2 * 148:
+        return 0
+    return 2 if -(-m // 256) * -(-n // 256) >= 74 else 1
+
+
 CONFIG_SHAPES = {
     "C0": (64, 800, 320),
     "C1": (128, 4096, 4096),

@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2101_05615_b200 as q8
+from configs import tile_class
 from paper_2101_05615_b200 import _lib
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -108,8 +109,9 @@ def test_needs_row_offsets_and_relu():
 def test_kernel_cache_builds_each_class_once_under_races():
     # test_dispatch.cpp:102-129 / acceptance.cpp:389-405
     kc = q8.KernelCache()
-    shapes = [(m, 64, 64, 64) for m in (1, 5, 28, 300)] + [(m, 64, 45, 45) for m in (1, 300)]
-    expected_classes = {(0 if m <= 256 else 1 if m <= 1024 else 2, k % 16 == 0, lda % 16 == 0) for m, _, k, lda in shapes}
+    shapes = ([(m, 64, 64, 64) for m in (1, 5, 28, 300)] + [(m, 64, 45, 45) for m in (1, 300)] +
+              [(2048, 1024, 64, 64), (4096, 11008, 64, 64)])
+    expected_classes = {(tile_class(m, n), k % 16 == 0, lda % 16 == 0) for m, n, k, lda in shapes}
 
     def race():
         for s in shapes:
@@ -122,8 +124,9 @@ def test_kernel_cache_builds_each_class_once_under_races():
         t.join()
     assert kc.build_count() == len(expected_classes)
     assert kc.tile(1, 64, 64, 64) == 1  # small-M tensor-core tile
-    assert kc.tile(300, 64, 64, 64) == 3  # mid-M 128-column tiles
-    assert kc.tile(3000, 64, 64, 64) == 2  # large-M persistent CTA-pair tiles
+    assert kc.tile(300, 64, 64, 64) == 1  # few tiles: split-K
+    assert kc.tile(2048, 1024, 4096, 4096) == 3  # 128-column tiles
+    assert kc.tile(4096, 11008, 4096, 4096) == 2  # persistent CTA-pair tiles
     assert kc.tile(300, 64, 45, 45) == 0  # TMA cannot address it: generic tile
     g = q8.KernelCache(generic_only=True)
     assert g.tile(300, 64, 64, 64) == 0

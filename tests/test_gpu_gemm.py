@@ -111,9 +111,10 @@ def test_tensor_core_paths_raw(cuda, orc, m, n, k):
     a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
     pw = q8.prepack_weights(b)
     kc = q8.KernelCache()
-    assert kc.tile(m, n, k, k) == (1 if m <= 256 else 3 if m <= 1024 else 2)
-    # launch families count tile widths: <= 128 columns (split-K, mid-M) vs 256 / pair tiles
-    fam = "gemm_tc_small_m" if m <= 1024 else "gemm_tc_large_m"
+    cls = configs.tile_class(m, n)
+    assert kc.tile(m, n, k, k) == {0: 1, 1: 3, 2: 2}[cls]
+    # launch families count tile widths: <= 128 columns (split-K, 128-column tiles) vs CTA-pair tiles
+    fam = "gemm_tc_large_m" if cls == 2 else "gemm_tc_small_m"
     before = q8.launch_stats()
     assert (run_raw(a, pw, cache=kc) == orc.naive_gemm_i32(a, b)).all()
     after = q8.launch_stats()
@@ -331,7 +332,8 @@ def test_large_m_pair_kernel_repeated_runs_exact(cuda, orc):
     # both TMEM accumulators cycling: raw accumulators vs the oracle, then 20
     # back-to-back requant + row-sum launches that must all equal the oracle
     # (a cross-CTA ordering race would show up as sporadic mismatches)
-    m = n = k = 2048
+    m, n, k = 2560, 2048, 1024  # 80 pair tiles >= 74 SM pairs: the pair kernel
+    assert configs.tile_class(m, n) == 2
     c = configs.gemm_case(orc, "C1", m, n, k, seed=2048)
     pw = q8.prepack_weights(c.b)
     acc = orc.naive_gemm_i32(c.a, c.b)
