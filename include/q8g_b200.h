@@ -65,7 +65,9 @@ int q8g_version(void);
 uint64_t q8g_launch_count(void);
 /* per kernel family: [0] pack, [1] GEMM CUDA-core, [2] GEMM tcgen05 small-M,
  * [3] GEMM tcgen05 large-M, [4] conv CUDA-core, [5] conv tcgen05,
- * [6] depthwise CUDA-core, [7] depthwise tcgen05, [8] general-pipeline post */
+ * [6] depthwise CUDA-core, [7] depthwise tcgen05, [8] general-pipeline post,
+ * [9] conv3x3 im2col (shapes the implicit-GEMM kernel cannot hold; the GEMM
+ *     launches count under [2] / [3]) */
 int q8g_launch_stats(uint64_t* counts, int n);
 /* debug (env Q8G_TC_TRACE set): 8 globaltimer stamps per CTA of the last
  * tensor-core GEMM launch; returns the number of CTA records copied.  With

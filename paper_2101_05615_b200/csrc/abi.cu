@@ -102,6 +102,10 @@ static int resolve_tile(q8g_kernel_cache* kc, int rows, int n, int k, bool align
     return kind;
 }
 
+int default_tile_kind(int rows, int n, int k, bool aligned) {
+    return resolve_tile(&process_cache(), rows, n, k, aligned);
+}
+
 static bool a_is_tma_aligned(const void* a, int lda) {
     return ((uintptr_t)a % 16 == 0) && (lda % 16 == 0);
 }

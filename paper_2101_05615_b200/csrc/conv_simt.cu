@@ -125,7 +125,14 @@ cudaError_t launch_conv3x3_simt(const ConvArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s) {
-    if (conv_tc_supported(a) && getenv("Q8G_CONV_SIMT") == nullptr) return launch_conv3x3_tc(a, s);
+    // implicit GEMM when its operands fit shared memory, else im2col + the
+    // tensor-core GEMM; the CUDA-core kernel when neither can run (no
+    // workspace during a capture).  Q8G_CONV_SIMT=1 forces it (A/B checks).
+    if (getenv("Q8G_CONV_SIMT") == nullptr) {
+        if (conv_tc_supported(a)) return launch_conv3x3_tc(a, s);
+        const cudaError_t e = launch_conv3x3_im2col(a, s);
+        if (e != cudaErrorNotSupported) return e;
+    }
     return launch_conv3x3_simt(a, s);
 }
 

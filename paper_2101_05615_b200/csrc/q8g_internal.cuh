@@ -47,8 +47,9 @@ enum KernelFamily : int {
     kFamConvTc = 5,
     kFamDw = 6,
     kFamDwTc = 7,
-    kFamPost = 8,  // general-pipeline post kernel (post.cu)
-    kFamCount = 9
+    kFamPost = 8,        // general-pipeline post kernel (post.cu)
+    kFamConvIm2col = 9,  // conv3x3 im2col for the GEMM path (conv_im2col.cu)
+    kFamCount = 10
 };
 void count_launch(int family);
 
@@ -218,6 +219,10 @@ struct ConvArgs {
     bool raw;
 };
 cudaError_t launch_conv3x3(const ConvArgs& a, cudaStream_t s);
+// im2col + tensor-core GEMM; cudaErrorNotSupported -> use the CUDA-core conv
+cudaError_t launch_conv3x3_im2col(const ConvArgs& a, cudaStream_t s);
+// the process dispatch cache's tile kind for a GEMM shape (abi.cu)
+int default_tile_kind(int rows, int n, int k, bool aligned);
 bool conv_tc_supported(const ConvArgs& a);
 cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s);
 

@@ -52,16 +52,16 @@ def test_conv3x3_small_vs_oracle(cuda, orc, shape):
 
 # conv_tc extremes: C in {32, 64, 128}, OC up to 240 (two 256-column TMEM
 # accumulators), the widest W (2 rows x (W+2) <= 128), odd H; ReLU on / off and
-# zp_c at both ends of the saturating-pack fast path.  The CUDA-core kernel
-# runs when the tile does not fit: W = 63, C = 48, or C = 128 with OC = 240
-# (operand image 294 KB > shared memory)
+# zp_c at both ends of the saturating-pack fast path.  im2col + the
+# tensor-core GEMM runs when the tile does not fit: W = 63, C = 48, or C = 128
+# with OC = 240 (operand image 294 KB > shared memory)
 @pytest.mark.parametrize("shape,relu,zp_c,fam", [((2, 5, 62, 32, 16), False, 0, "conv_tc"),
                                                  ((1, 7, 20, 64, 240), True, 255, "conv_tc"),
                                                  ((1, 5, 9, 128, 112), False, 3, "conv_tc"),
                                                  ((3, 4, 11, 64, 112), False, 255, "conv_tc"),
-                                                 ((1, 2, 63, 32, 32), True, 5, "conv_simt"),
-                                                 ((1, 3, 8, 48, 32), False, 9, "conv_simt"),
-                                                 ((1, 3, 6, 128, 240), True, 5, "conv_simt")])
+                                                 ((1, 2, 63, 32, 32), True, 5, "conv_im2col"),
+                                                 ((1, 3, 8, 48, 32), False, 9, "conv_im2col"),
+                                                 ((1, 3, 6, 128, 240), True, 5, "conv_im2col")])
 def test_conv3x3_edge_shapes_vs_oracle(cuda, orc, shape, relu, zp_c, fam):
     import dataclasses
     nb, h, w, c, oc = shape
@@ -155,3 +155,31 @@ def test_dwconv_c4_full_vs_oracle(cuda, orc):
         q8.execute_dwconv3x3(xd, f, y2, image_begin=i0, image_end=i1)
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
+
+
+# im2col + tensor-core GEMM: the channel counts real networks use beyond the
+# implicit-GEMM kernel (256, 512), odd C (byte-wise im2col, K padded to 16),
+# OC > 240, and the CUDA-core kernel forced for the same shapes
+@pytest.mark.parametrize("shape", [(2, 14, 14, 256, 256), (1, 7, 7, 512, 128), (2, 9, 11, 3, 64),
+                                   (1, 6, 5, 17, 300), (4, 28, 28, 256, 64)])
+def test_conv3x3_im2col_gemm_vs_oracle(cuda, orc, shape, monkeypatch):
+    nb, h, w, c, oc = shape
+    cc = configs.conv_case(orc, nb, h, w, c, oc, seed=7 * sum(shape))
+    pw = q8.prepack_conv3x3_weights(cc.w)
+    acc, exp = conv_oracle(orc, cc)
+    before = q8.launch_stats()
+    y = torch.zeros((nb, h, w, oc), dtype=torch.uint8, device="cuda")
+    q8.execute_conv3x3(dev(cc.x), pw, y, conv_pipeline(cc, c))
+    yr = torch.zeros((nb, h, w, oc), dtype=torch.int32, device="cuda")
+    q8.execute_conv3x3(dev(cc.x), pw, yr, q8.OutputPipeline([q8.WriteRawI32()]), zp_a=cc.zp_a)
+    torch.cuda.synchronize()
+    after = q8.launch_stats()
+    assert after["conv_im2col"] == before["conv_im2col"] + 2 and after["conv_simt"] == before["conv_simt"]
+    assert (y.cpu().numpy().reshape(-1, oc) == exp).all()
+    assert (yr.cpu().numpy().reshape(-1, oc) == acc).all()
+    monkeypatch.setenv("Q8G_CONV_SIMT", "1")
+    ys = torch.zeros_like(y)
+    q8.execute_conv3x3(dev(cc.x), pw, ys, conv_pipeline(cc, c))
+    torch.cuda.synchronize()
+    assert q8.launch_stats()["conv_simt"] == after["conv_simt"] + 1
+    assert torch.equal(ys, y)
