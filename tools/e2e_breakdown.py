@@ -97,5 +97,44 @@ def main():
     print(f"host-view call (event span): {full:.1f} us   wall clock per call: {wall:.1f} us")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--timeline" not in sys.argv:
     main()
+
+
+def overlap_timeline():
+    """Events around an H2D on one stream and a GEMM on another, both issued
+    right after a common start event: do they run concurrently?"""
+    m, n, k = 128, 4096, 4096
+    b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device="cuda")
+    pw = q8.prepack_weights(b)
+    rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=k, zp_b_per_channel=np.zeros(n, np.int32) + 3,
+                          multiplier_f32_per_channel=np.full(n, 1e-4, np.float32), rounding=q8.ROUND_F32_RNE)
+    pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])  # owns the epilogue
+    ep = pipe.epilogue(pw)
+    lib = _lib.load()
+    s, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a_h = torch.randint(0, 256, (m, k), dtype=torch.uint8).pin_memory()
+    a_d = torch.empty((m, k), dtype=torch.uint8, device="cuda")
+    a_d2 = torch.empty((m, k), dtype=torch.uint8, device="cuda")
+    c_d = torch.empty((m, n), dtype=torch.uint8, device="cuda")
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for it in range(6):
+        ev0, c0, c1, g0, g1 = E(), E(), E(), E(), E()
+        ev0.record(s)
+        s2.wait_event(ev0)
+        c0.record(s2)
+        with torch.cuda.stream(s2):
+            a_d2.copy_(a_h, non_blocking=True)
+        c1.record(s2)
+        g0.record(s)
+        _lib.check(lib.q8g_gemm_u8s8_requant(a_d.data_ptr(), m, k, k, pw.handle, ep, c_d.data_ptr(), n, 0, m, None,
+                                             s.cuda_stream))
+        g1.record(s)
+        torch.cuda.synchronize()
+        if it >= 3:
+            print(f"copy {ev0.elapsed_time(c0)*1e3:6.1f} -> {ev0.elapsed_time(c1)*1e3:6.1f} us   "
+                  f"gemm {ev0.elapsed_time(g0)*1e3:6.1f} -> {ev0.elapsed_time(g1)*1e3:6.1f} us")
+
+
+if __name__ == "__main__" and "--timeline" in sys.argv:
+    overlap_timeline()
