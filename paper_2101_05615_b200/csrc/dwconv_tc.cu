@@ -385,7 +385,7 @@ constexpr int KG = CB / 32; // K-groups of 32 channels
 constexpr int N2 = 64;      // MMA N: 32 outputs + 32 zero-point columns
 
 struct Dw2Layout {
-    int halo_off, halo_stride, b_off, corr_off, mult_off, bar_off, tmemptr_off, total;
+    int halo_off, halo_stride, b_off, corr_off, mult_off, out_off, out_stride, bar_off, tmemptr_off, total;
 };
 __host__ __device__ inline Dw2Layout dw2_layout(int wp) {
     Dw2Layout L;
@@ -394,7 +394,10 @@ __host__ __device__ inline Dw2Layout dw2_layout(int wp) {
     L.b_off = L.halo_off + NB2 * L.halo_stride;
     L.corr_off = L.b_off + 9 * KG * 2048;  // B: [tap][K-group][K half][64 rows][16 B]
     L.mult_off = L.corr_off + 16 * CB * 4;  // [16 classes][64] int32: cterm + border correction
-    L.bar_off = L.mult_off + CB * 4;
+    // output tiles for the TMA store, double-buffered: [R2 rows][W][64 B], SWIZZLE_64B
+    L.out_off = align_up(L.mult_off + CB * 4, 1024);
+    L.out_stride = align_up(R2 * (wp - 2) * CB, 1024);
+    L.bar_off = L.out_off + 2 * L.out_stride;
     L.tmemptr_off = L.bar_off + (2 * NB2 + 4) * 8;
     L.total = L.tmemptr_off + 16 + 1024;
     return L;
@@ -413,7 +416,8 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
 }
 
 __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
-    dwconv_tc64_kernel(const __grid_constant__ CUtensorMap tmap_x, const DwParams p) {
+    dwconv_tc64_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
+                       const DwParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     const uint32_t base = (raw_addr + 1023u) & ~1023u;
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_x);
+        ptx::prefetch_tmap(&tmap_y);
         for (int b = 0; b < NB2; ++b) {
             ptx::mbar_init(full_bar(b), 1);
             ptx::mbar_init(empty_bar(b), 1);
@@ -551,17 +556,26 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         const float magic = 12582912.0f;  // 1.5 * 2^23 (cterm carries its bit pattern)
         const float floor_x = p.lo == 0.0f ? 0.0f : -8388608.0f;  // ReLU: 0; else -2^23 (see conv_tc.cu)
         const int32_t zoff = 0x4B400000 - p.zp_c;
+        // the unit's 2 x W x 64 output bytes go to a shared-memory tile and out
+        // with one 4-D TMA store (64-byte rows, like the halo) instead of four
+        // 16-byte stores per thread scattered at the C-byte position stride
+        const bool storer = ew == 0 && lane == 0;
         int acc = 0;
         uint32_t aph = 0;
-        for (int k = cta_in; k < p.units_blk; k += ctas) {
-            const int n = k / p.rb2, oh = (k % p.rb2) * R2 + r;
+        int ui = 0;
+        for (int k = cta_in; k < p.units_blk; k += ctas, ++ui) {
+            const int n = k / p.rb2, oh0 = (k % p.rb2) * R2, oh = oh0 + r;
             const bool valid = oh < p.h && ocol >= 0 && ocol < p.w;
             const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
+            uint8_t* tile = smem + L.out_off + (ui & 1) * L.out_stride;
+            // the store issued from this buffer two units ago has read it
+            if (storer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI_WARPS) : "memory");
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
-            if (ew == 0 && lane == 0) dw_stamp(p, 3, (k - cta_in) / ctas);
+            if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
             const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + r * KG * N2);
-            uint8_t* dst = p.y + ((((size_t)n * p.h + oh) * p.w + ocol) * p.c + c0);
+            const int q = r * p.w + ocol;  // 64-byte row of the tile (SWIZZLE_64B: chunk ^= (q >> 1) & 3)
 #pragma unroll
             for (int j = 0; j < KG; ++j) {
                 uint32_t vw[32], vz[32];
@@ -588,20 +602,34 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                     }
                     w8[g] = pack_sat_u8(rr[1], rr[0], pack_sat_u8(rr[3], rr[2], 0u));
                 }
-                if (valid) {
-                    reinterpret_cast<uint4*>(dst + j * 32)[0] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
-                    reinterpret_cast<uint4*>(dst + j * 32)[1] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+                if (ocol >= 0 && ocol < p.w) {
+                    uint4* row16 = reinterpret_cast<uint4*>(tile + (size_t)q * 64);
+                    row16[(2 * j) ^ ((q >> 1) & 3)] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+                    row16[(2 * j + 1) ^ ((q >> 1) & 3)] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
                 }
             }
+            (void)valid;
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
-            if (ew == 0 && lane == 0) dw_stamp(p, 4, (k - cta_in) / ctas);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile writes -> TMA
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+            if (storer) {
+                // rows past H are clipped by the tensor map
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmap_y)),
+                    "r"(c0), "r"(0), "r"(oh0), "r"(n), "r"(ptx::smem_u32(tile))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                dw_stamp(p, 4, ui);
+            }
             if (++acc == 2) {
                 acc = 0;
                 aph ^= 1;
             }
         }
+        if (storer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // smem stays valid until stored
     }
 
     __syncwarp();
@@ -643,6 +671,15 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
             CU_TENSOR_MAP_INTERLEAVE_NONE, tc64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
+    // output map (64-channel kernel): TMA store of [R2 rows][W][64 ch] tiles
+    CUtensorMap tmap_y;
+    if (tc64) {
+        cuuint32_t boxy[4] = {(cuuint32_t)CB, (cuuint32_t)w, (cuuint32_t)R2, 1};
+        if (enc(&tmap_y, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, y, dims, strides, boxy, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
     DwParams p;
     p.nb = nb;
     p.h = h;
@@ -681,7 +718,7 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
         if (per_blk < 1) per_blk = 1;
         if (per_blk > p.units_blk) per_blk = p.units_blk;
         const cudaError_t e = launch_with_pdl(dwconv_tc64_kernel, dim3(per_blk * p.nblk), dim3(128 + 32 * EPI_WARPS),
-                                              dw2_layout(p.wp).total, s, tmap, p);
+                                              dw2_layout(p.wp).total, s, tmap, tmap_y, p);
         count_launch(kFamDwTc);
         return e;
     }
