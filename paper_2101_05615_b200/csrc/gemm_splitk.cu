@@ -207,7 +207,10 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     // in flight can be writing them; A may be the previous grid's output and
     // is only loaded after griddepcontrol.wait.
     const int nkl = kb1 - kb0;  // this rank's k-blocks
-    const int npre = nkl < BST ? nkl : BST;
+    // at most 4 stages before the PDL wait, the rest right after it: fewer
+    // requests in the entry burst land the first stage sooner (C1: 7.9 vs
+    // 8.25 us per step with all 6 up front; 3 or 5: 8.0-8.1)
+    const int npre = nkl < (BST < 4 ? BST : 4) ? nkl : (BST < 4 ? BST : 4);
     const uint64_t pol_b = ptx::policy_evict_first();  // weights streamed once
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < BST; ++s) {
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 sk_kb(p, 0, j);
             }
             __syncwarp();
-            if (j >= npre) {  // B slots are reused only when the slice exceeds BST k-blocks
+            if (j >= npre) {  // stages not requested at entry: fresh slots first, then reused ones
                 ptx::mbar_wait(bempty_bar(sb), ((uint32_t)(j / BST) & 1u) ^ 1u);
                 if (ptx::elect_one()) {
                     ptx::mbar_arrive_expect_tx(bfull_bar(sb), Cfg::B_STAGE);
