@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -703,7 +704,7 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
     const int lda_d = round_up_i(k, 16), ldc_d = pb->n;
     // grow-only per-device staging buffers; host-view calls are synchronous
     // and serialised per device by this lock.  A is copied on a separate
-    // stream that ends with a stream write of the call's epoch to `flag`: the
+    // stream followed by a copy of the call's epoch into `flag`: the
     // GEMM is launched at the same time and streams the (immutable) weights
     // while A is in flight (the split-K kernel polls the flag before its first
     // A load; other kernels wait on it in-stream).
@@ -715,6 +716,8 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
         cudaStream_t copy = nullptr;
         uint32_t* flag = nullptr;
         uint32_t epoch = 0;
+        cudaEvent_t done = nullptr;  // spin-waited (no BlockingSync): low wake-up latency
+        uint32_t* epoch_host = nullptr;  // pinned source of the flag copy
     };
     static Staging staging[64];
     Staging& st = staging[pb->device & 63];
@@ -741,15 +744,29 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
         if ((e = cudaMalloc(&st.flag, sizeof(uint32_t))) != cudaSuccess ||
             (e = cudaMemsetAsync(st.flag, 0, sizeof(uint32_t), st.copy)) != cudaSuccess)
             return cuda_fail(e, "A-ready flag");
+        if ((e = cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "completion event");
+        if ((e = cudaHostAlloc(&st.epoch_host, sizeof(uint32_t), cudaHostAllocDefault)) != cudaSuccess)
+            return cuda_fail(e, "pinned epoch");
     }
     uint32_t epoch = ++st.epoch;
     if (epoch == 0) epoch = ++st.epoch;
     uint8_t* d_a = (uint8_t*)st.a;
     OutT* d_c = (OutT*)st.c;
     int rc = Q8G_OK;
-    e = cudaMemcpy2DAsync(d_a, lda_d, a_host + (size_t)row_begin * lda, lda, k, rows,
-                          cudaMemcpyHostToDevice, st.copy);
-    if (e == cudaSuccess) e = stream_write_u32(st.copy, st.flag, epoch);
+    // contiguous rows: one linear copy
+    if (lda == k && lda_d == k)
+        e = cudaMemcpyAsync(d_a, a_host + (size_t)row_begin * lda, (size_t)rows * k, cudaMemcpyHostToDevice, st.copy);
+    else
+        e = cudaMemcpy2DAsync(d_a, lda_d, a_host + (size_t)row_begin * lda, lda, k, rows, cudaMemcpyHostToDevice,
+                              st.copy);
+    // the flag is written by the same copy stream right behind A (a 4-byte
+    // copy from pinned memory, ordered after A's bytes).  Reusing the pinned
+    // word is safe: calls are synchronous, so the previous call's flag copy
+    // has completed.
+    *st.epoch_host = epoch;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(st.flag, st.epoch_host, sizeof(uint32_t), cudaMemcpyHostToDevice, st.copy);
+
     if (e != cudaSuccess) rc = cuda_fail(e, "H2D A");
     if (!rc) {
         if (raw)
@@ -761,10 +778,16 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
     }
     if (rc) cudaStreamSynchronize(st.copy);  // never leave the copy in flight into freed staging
     if (!rc) {
-        e = cudaMemcpy2DAsync(c_host + (size_t)row_begin * ldc, sizeof(OutT) * ldc, d_c,
-                              sizeof(OutT) * ldc_d, sizeof(OutT) * pb->n, rows,
-                              cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (ldc == pb->n && ldc_d == pb->n)
+            e = cudaMemcpyAsync(c_host + (size_t)row_begin * ldc, d_c, sizeof(OutT) * (size_t)rows * pb->n,
+                                cudaMemcpyDeviceToHost, s);
+        else
+            e = cudaMemcpy2DAsync(c_host + (size_t)row_begin * ldc, sizeof(OutT) * ldc, d_c, sizeof(OutT) * ldc_d,
+                                  sizeof(OutT) * pb->n, rows, cudaMemcpyDeviceToHost, s);
+        // the call is synchronous: spin on an event (cudaStreamSynchronize
+        // may yield the thread and wake up several us late)
+        if (e == cudaSuccess) e = cudaEventRecord(st.done, s);
+        if (e == cudaSuccess) e = cudaEventSynchronize(st.done);
         if (e != cudaSuccess) rc = cuda_fail(e, "D2H C");
     }
     return rc;
