@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 ph ^= 1;
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 || warp == 3) {
         // ------------------------------------------------ MMA issuer
         // The whole warp runs the loop (warp-uniform control flow) and one
         // elected lane issues: every descriptor is then a uniform-register
@@ -323,11 +323,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         const uint64_t bstep = (uint64_t)(2 * p.nq);       // one (tap, K-step) block of B: 2 halves x nq rows x 16 B
         const uint64_t b0 = kmajor_noswz_desc(base + L.b_off, (uint32_t)(p.nq * 16), 128);
         const uint64_t a0 = kmajor_swz_desc(0u, p.c);
-        int b = 0, acc = 0;
-        uint32_t ph = 0, aph = 0;
+        // two issuing warps on different SMSPs (1 and 3) take alternate units:
+        // each shares its SMSP with an epilogue warp, and a busy neighbour
+        // delays a warp's next issue (tools/mma_desc.cu); with two, one of
+        // them usually has the next unit's MMAs queued
+        const int q = warp == 1 ? 0 : 1;
         ptx::mbar_wait(img_bar, 0);
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-            const int ui = (u - (int)blockIdx.x) / (int)gridDim.x;
+        int ui = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
+            if ((ui & 1) != q) continue;
+            const int b = ui % p.nbuf, acc = ui % p.nacc;
+            const uint32_t ph = (uint32_t)(ui / p.nbuf) & 1u, aph = (uint32_t)(ui / p.nacc) & 1u;
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
             if (lane == 0) cv_stamp(p, 5, ui);
             ptx::mbar_wait(full_bar(b), ph);
@@ -349,14 +355,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 cv_stamp(p, 2, ui);
             }
             __syncwarp();
-            if (++b == p.nbuf) {
-                b = 0;
-                ph ^= 1;
-            }
-            if (++acc == p.nacc) {
-                acc = 0;
-                aph ^= 1;
-            }
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
