@@ -51,7 +51,7 @@ struct SkCfg {
     static constexpr int OWN = BN / S;  // columns owned per rank
     static constexpr int B_STAGE = BN * kKBlock;
     static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;  // one accumulator tile
-    // one exchange slot: partials [OWN/4 quads][BM rows] int4, then [BM] row sums
+    // one exchange slot: partials [OWN/8 octs][BM rows] 32 B (256-bit accesses), then [BM] row sums
     static constexpr int SLOT_PART = (OWN / 4) * BM * 16;
     static constexpr int SLOT_BYTES = SLOT_PART + BM * 4;
     static constexpr int A_OFF = 0;
