@@ -385,3 +385,50 @@ def test_c2_full_size_row_subset_vs_oracle(cuda, orc):
     colsum_exact = rs @ c.b.astype(np.int64)
     # raw int32 accumulators are exact (|acc| < 2^31 at K = 4096)
     assert (colsum_gpu == colsum_exact).all()
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_requant_fuzz_vs_oracle(cuda, orc, seed):
+    """Random shapes (every tile class, K % 16 != 0 -> generic kernel), both
+    rounding modes, per-tensor / per-channel, ReLU, bias, zero points over
+    their whole range, a wider A leading dimension and 1-3 worker stripes,
+    bit-exact against the oracle's requant (quant.hpp:115-133)."""
+    rng = np.random.default_rng(1000 + seed)
+    m = int(rng.choice([1, 3, 17, 64, 128, 129, 200, 300, 513, 1100]))
+    n = int(rng.choice([1, 7, 16, 33, 128, 255, 256, 700]))
+    k = int(rng.choice([1, 5, 16, 64, 100, 128, 384, 640, 1024]))
+    r = orc.rng(seed)
+    a, b = r.u8_matrix(m, k), r.i8_matrix(k, n)
+    per_channel, relu = bool(rng.integers(2)), bool(rng.integers(2))
+    rounding = int(rng.integers(2))
+    zp_a, zp_c = int(rng.integers(0, 256)), int(rng.integers(0, 256))
+    bias = rng.integers(-5000, 5001, n).astype(np.int32) if rng.integers(2) else None
+    if per_channel:
+        zp_b = rng.integers(-20, 21, n).astype(np.int32)
+        mult = rng.uniform(1e-5, 1e-2, n)
+    else:
+        zp_b = int(rng.integers(-20, 21))
+        mult = float(rng.uniform(1e-5, 1e-2))
+    rp = q8.RequantParams(multiplier=1.0 if per_channel else mult, zp_a=zp_a, zp_b=0 if per_channel else zp_b,
+                          zp_c=zp_c, k_total=k, bias=bias, rounding=rounding)
+    if per_channel:
+        rp.zp_b_per_channel = zp_b
+        if rounding == q8.ROUND_F32_RNE:
+            rp.multiplier_f32_per_channel = mult.astype(np.float32)
+        else:
+            rp.multiplier_per_channel = mult
+    pipe = q8.OutputPipeline(([q8.ReluQuantized()] if relu else []) + [q8.Requantize(rp)])
+    pw = q8.prepack_weights(b)
+    pad = int(rng.choice([0, 16, 48]))
+    a_wide = torch.zeros((m, k + pad), dtype=torch.uint8, device="cuda")
+    a_wide[:, :k] = dev(a)
+    out = torch.full((m, n), 7, dtype=torch.uint8, device="cuda")
+    nt = int(rng.integers(1, 4))
+    for t in rng.permutation(nt):
+        q8.execute_gemm(a_wide[:, :k], pw, out, pipe, thread_id=int(t), num_threads=nt)
+    torch.cuda.synchronize()
+    acc = orc.naive_gemm_i32(a, b)
+    exp = orc.requant_matrix(acc, orc.row_offsets(a), orc.col_offsets(b), zp_a, zp_b, k, bias, rounding,
+                             mult if per_channel else mult, zp_c, relu, per_channel=per_channel)
+    got = out.cpu().numpy()
+    assert (got == exp).all(), (m, n, k, per_channel, relu, rounding, int((got != exp).sum()))
