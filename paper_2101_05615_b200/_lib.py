@@ -144,7 +144,7 @@ def launch_count() -> int:
 
 
 FAMILIES = ("pack", "gemm_simt", "gemm_tc_small_m", "gemm_tc_large_m", "conv_simt", "conv_tc", "dw_simt",
-            "dw_tc", "post", "conv_im2col")
+            "dw_tc", "post", "conv_im2col", "dw_fma")
 
 
 def launch_stats() -> dict:

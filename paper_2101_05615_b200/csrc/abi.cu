@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -921,6 +922,7 @@ int q8g_dw_filter_create(const int8_t* w_host, int c, const q8g_requant_params* 
             }
         }
         // |adj| <= 9 * 255 * (128 + |zp_w|) + |bias| must stay below 2^22
+        const bool ok_fma = ok;  // the FMA path has its own bias bound (below)
         if (9LL * 255 * 256 + max_bias >= (1LL << 22)) ok = false;
         f->lo = p->relu ? 0.0f : (float)(-p->zp_c);
         f->hi = (float)(255 - p->zp_c);
@@ -940,6 +942,38 @@ int q8g_dw_filter_create(const int8_t* w_host, int c, const q8g_requant_params* 
             }
             f->tc_ok = true;
         }
+        // ---- CUDA-core FMA path constants (dwconv_fma.cu).  Exactness: every
+        // partial sum bias' + sum x*w' is an integer below 2^23 (|w'| <= 255),
+        // mult * 2^30 is finite, and the magic-number requant needs
+        // 0 <= zp_c <= 255
+        const int64_t fma_bound = max_bias + 2LL * 9 * 255 * 255;
+        if (ok_fma && c % 4 == 0 && fma_bound < (1LL << 23)) {
+            std::vector<float> fw((size_t)9 * c), fb(c), fm(c), fc((size_t)16 * c);
+            for (int ch = 0; ch < c; ++ch) {
+                int64_t ws = 0;
+                for (int t = 0; t < 9; ++t) {
+                    const int wp = (int)w_host[t * c + ch] - zpw[ch];
+                    ws += wp;
+                    fw[((size_t)(ch / 4) * 9 + t) * 4 + ch % 4] = std::ldexp((float)wp, 119);
+                }
+                const int64_t b = p->bias_host ? p->bias_host[ch] : 0;
+                fb[ch] = std::ldexp((float)(b - (int64_t)p->zp_a * ws), -30);
+                fm[ch] = std::ldexp(mult[ch], 30);
+                for (int cls = 0; cls < 16; ++cls) fc[(size_t)cls * c + ch] = std::ldexp((float)corr[cls * c + ch], -30);
+            }
+            if ((e = cudaMalloc(&f->fma_w, sizeof(float) * 9 * c)) != cudaSuccess ||
+                (e = cudaMalloc(&f->fma_b, sizeof(float) * c)) != cudaSuccess ||
+                (e = cudaMalloc(&f->fma_m, sizeof(float) * c)) != cudaSuccess ||
+                (e = cudaMalloc(&f->fma_corr, sizeof(float) * 16 * c)) != cudaSuccess ||
+                (e = cudaMemcpy(f->fma_corr, fc.data(), sizeof(float) * 16 * c, cudaMemcpyHostToDevice)) !=
+                    cudaSuccess ||
+                (e = cudaMemcpy(f->fma_w, fw.data(), sizeof(float) * 9 * c, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(f->fma_b, fb.data(), sizeof(float) * c, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(f->fma_m, fm.data(), sizeof(float) * c, cudaMemcpyHostToDevice)) != cudaSuccess) {
+                q8g_dw_filter_free(f);
+                return cuda_fail(e, "dw_filter FMA tables");
+            }
+        }
     }
     *out = f;
     return Q8G_OK;
@@ -954,6 +988,10 @@ int q8g_dw_filter_free(q8g_dw_filter* f) {
     if (f->cterm_dev) cudaFree(f->cterm_dev);
     if (f->mult_dev) cudaFree(f->mult_dev);
     if (f->corr_dev) cudaFree(f->corr_dev);
+    if (f->fma_w) cudaFree(f->fma_w);
+    if (f->fma_b) cudaFree(f->fma_b);
+    if (f->fma_m) cudaFree(f->fma_m);
+    if (f->fma_corr) cudaFree(f->fma_corr);
     delete f;
     return Q8G_OK;
 }

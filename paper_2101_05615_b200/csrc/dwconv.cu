@@ -83,8 +83,18 @@ __global__ void dw_scalar_kernel(const uint8_t* __restrict__ x, int nb, int h, i
 
 cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c, const q8g_dw_filter* f,
                              uint8_t* y, cudaStream_t s) {
-    if (f->tc_ok && dw_tc_supported(h, w, c, f->zp_a) && getenv("Q8G_DW_SIMT") == nullptr)
-        return launch_dwconv3x3_tc(x, nb, h, w, c, f, y, s);
+    // order: the 64-channel tensor-core kernel (fastest where it fits: W + 2 <= 128),
+    // the FMA-pipe kernel (C % 128 == 0, any width), the 16-channel tensor-core
+    // kernel, the plain CUDA-core kernel.  A/B switches: Q8G_DW_SIMT forces the
+    // last; Q8G_DW_FMA=1 / =0 forces / disables the FMA-pipe kernel.
+    const bool simt = getenv("Q8G_DW_SIMT") != nullptr;
+    const char* fenv = getenv("Q8G_DW_FMA");
+    const bool fma_ok = !simt && f->fma_w && dw_fma_supported(h, w, c) && !(fenv && fenv[0] == '0');
+    const bool tc_ok = !simt && f->tc_ok && dw_tc_supported(h, w, c, f->zp_a);
+    if (fma_ok && fenv && fenv[0] == '1') return launch_dwconv3x3_fma(x, nb, h, w, c, f, y, s);
+    if (tc_ok && dw_tc64_supported(w, c)) return launch_dwconv3x3_tc(x, nb, h, w, c, f, y, s);
+    if (fma_ok) return launch_dwconv3x3_fma(x, nb, h, w, c, f, y, s);
+    if (tc_ok) return launch_dwconv3x3_tc(x, nb, h, w, c, f, y, s);
     int dev = 0;
     cudaGetDevice(&dev);
     const int blocks = sm_count(dev) * 8;

@@ -648,6 +648,8 @@ bool dw_tc64_ok(int w, int c) {
 
 }  // namespace
 
+bool dw_tc64_supported(int w, int c) { return tmap_encoder() != nullptr && dw_tc64_ok(w, c); }
+
 bool dw_tc_supported(int h, int w, int c, int32_t zp_a) {
     (void)zp_a;
     if (h < 1 || tmap_encoder() == nullptr) return false;

@@ -49,7 +49,8 @@ enum KernelFamily : int {
     kFamDwTc = 7,
     kFamPost = 8,        // general-pipeline post kernel (post.cu)
     kFamConvIm2col = 9,  // conv3x3 im2col for the GEMM path (conv_im2col.cu)
-    kFamCount = 10
+    kFamDwFma = 10,      // depthwise on the CUDA-core FMA pipes (dwconv_fma.cu)
+    kFamCount = 11
 };
 void count_launch(int family);
 
@@ -138,6 +139,11 @@ struct q8g_dw_filter {
     float* mult_dev = nullptr;       // [c]
     int32_t* corr_dev = nullptr;     // [16][c] zero-padding corrections per border class
     float lo = 0.f, hi = 255.f;      // clamp bounds before + zp_c
+    // CUDA-core FMA path (dwconv_fma.cu); null -> not exact for these params
+    float* fma_w = nullptr;          // [c/4][9][4]: (w - zp_w) * 2^119
+    float* fma_b = nullptr;          // [c]: (bias - zp_a * sum_t (w - zp_w)) * 2^-30
+    float* fma_m = nullptr;          // [c]: mult * 2^30
+    float* fma_corr = nullptr;       // [16][c]: corr * 2^-30 (zero-fill border classes)
 };
 
 namespace q8g {
@@ -229,6 +235,10 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s);
 cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c,
                              const q8g_dw_filter* f, uint8_t* y, cudaStream_t s);
 bool dw_tc_supported(int h, int w, int c, int32_t zp_a);
+bool dw_fma_supported(int h, int w, int c);
+bool dw_tc64_supported(int w, int c);
+cudaError_t launch_dwconv3x3_fma(const uint8_t* x, int nb, int h, int w, int c, const q8g_dw_filter* f,
+                                 uint8_t* y, cudaStream_t s);
 cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, const q8g_dw_filter* f,
                                 uint8_t* y, cudaStream_t s);
 

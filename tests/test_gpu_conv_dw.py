@@ -110,6 +110,8 @@ def test_dwconv_small_vs_oracle(cuda, orc, shape):
     assert (y.cpu().numpy() == exp).all()
 
 
+# dwconv_fma (C % 128 == 0, W + 2 > 128): 56-position segments with a
+# partial last segment, ragged row chunks;
 # dwconv_tc64 (C % 64 == 0, W + 2 <= 128): one / several channel blocks, odd H
 # (tail row block), W = 1 and the widest W; the 16-channel kernel for C % 64
 # != 0; the CUDA-core kernel when a 16-channel unit no longer fits one TMEM
@@ -119,7 +121,9 @@ def test_dwconv_small_vs_oracle(cuda, orc, shape):
                                                  ((1, 2, 1, 192), True, 200, "dw_tc"),
                                                  ((2, 4, 30, 48), False, 17, "dw_tc"),
                                                  ((1, 3, 200, 64), True, 5, "dw_simt"),
-                                                 ((4, 7, 13, 256), False, 128, "dw_tc")])
+                                                 ((4, 7, 13, 256), False, 128, "dw_tc"),
+                                                 ((1, 14, 300, 128), True, 9, "dw_fma"),
+                                                 ((2, 17, 127, 256), False, 3, "dw_fma")])
 def test_dwconv_tc_edge_shapes_vs_oracle(cuda, orc, shape, relu, zp_c, fam):
     import dataclasses
     nb, h, w, c = shape
@@ -139,6 +143,62 @@ def test_dwconv_tc_edge_shapes_vs_oracle(cuda, orc, shape, relu, zp_c, fam):
             q8.execute_dwconv3x3(xd, f, y2, image_begin=i0, image_end=i1)
         torch.cuda.synchronize()
         assert torch.equal(y, y2)
+
+
+# the FMA-pipe kernel forced (Q8G_DW_FMA=1) on shapes the tensor-core kernel
+# takes by default: row chunks of 14 with ragged tails, 56-position segments
+# with partial last segments, several channel blocks, H = W = 1; both kernels
+# agree bit for bit with the oracle
+@pytest.mark.parametrize("shape,relu,zp_c", [((2, 9, 126, 128), False, 255), ((3, 17, 56, 256), True, 5),
+                                             ((1, 1, 1, 128), True, 5), ((3, 29, 57, 128), True, 0),
+                                             ((2, 15, 112, 384), False, 77), ((1, 2, 5, 128), True, 200)])
+def test_dwconv_fma_vs_tc_same_bits(cuda, orc, shape, relu, zp_c, monkeypatch):
+    import dataclasses
+    nb, h, w, c = shape
+    dc = dataclasses.replace(configs.dw_case(orc, nb, h, w, c, seed=11 * sum(shape)), relu=relu, zp_c=zp_c)
+    exp, _ = orc.dwconv3x3(dc.x, dc.zp_a, dc.w, dc.zp_w, dc.bias, dc.mult_f32, dc.zp_c, dc.relu)
+    f = dw_filter(dc)
+    xd = dev(dc.x)
+    y = torch.zeros(shape, dtype=torch.uint8, device="cuda")
+    before = q8.launch_stats()
+    q8.execute_dwconv3x3(xd, f, y)
+    monkeypatch.setenv("Q8G_DW_FMA", "1")
+    yf = torch.zeros_like(y)
+    q8.execute_dwconv3x3(xd, f, yf)
+    torch.cuda.synchronize()
+    after = q8.launch_stats()
+    assert after["dw_fma"] == before["dw_fma"] + 1 and after["dw_tc"] == before["dw_tc"] + 1
+    assert (y.cpu().numpy() == exp).all()
+    assert torch.equal(y, yf)
+
+
+# the FMA kernel's exactness limits: extreme bytes and weights, zp_w at
+# +-127 (|w - zp_w| = 255), zp_a at 0 / 255, the largest admitted bias, huge
+# multipliers (saturation both ways), tiny and denormal-range multipliers,
+# zp_c at both ends, ReLU on and off
+@pytest.mark.parametrize("variant", range(6))
+def test_dwconv_fma_extremes_vs_oracle(cuda, orc, variant):
+    nb, h, w, c = 2, 16, 130, 128  # W + 2 > 128: the FMA-pipe kernel by default
+    r = np.random.default_rng(1000 + variant)
+    choice = lambda vals, size: r.choice(np.asarray(vals), size=size)  # noqa: E731
+    x = choice([0, 1, 127, 128, 254, 255], (nb, h, w, c)).astype(np.uint8)
+    wt = choice([-128, -127, -1, 0, 1, 126, 127], (3, 3, c)).astype(np.int8)
+    zp_w = choice([-127, -10, 0, 10, 127], c).astype(np.int32)
+    zp_a = [0, 255, 128, 3, 200, 128][variant]
+    big = (1 << 23) - 2 * 9 * 255 * 255 - 1
+    bias = r.integers(-big, big + 1, c).astype(np.int32)
+    bias[:4] = [big, -big, 0, big]
+    mult = [r.uniform(1e-7, 1e-5, c), r.uniform(1e-4, 1e-2, c), np.full(c, 3.0e5), r.uniform(1e-38, 1e-30, c),
+            r.uniform(0.5, 2.0, c), 10.0 ** r.uniform(-9, 4, c)][variant].astype(np.float32)
+    zp_c, relu = [(0, False), (255, True), (5, True), (128, False), (0, True), (17, False)][variant]
+    dc = configs.DwCase(x, wt, bias, zp_a, zp_w, mult, zp_c, relu)
+    exp, _ = orc.dwconv3x3(dc.x, dc.zp_a, dc.w, dc.zp_w, dc.bias, dc.mult_f32, dc.zp_c, dc.relu)
+    before = q8.launch_stats()["dw_fma"]
+    y = torch.zeros(x.shape, dtype=torch.uint8, device="cuda")
+    q8.execute_dwconv3x3(dev(x), dw_filter(dc), y)
+    torch.cuda.synchronize()
+    assert q8.launch_stats()["dw_fma"] == before + 1
+    assert (y.cpu().numpy() == exp).all()
 
 
 def test_dwconv_c4_full_vs_oracle(cuda, orc):
