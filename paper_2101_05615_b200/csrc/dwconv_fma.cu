@@ -23,7 +23,9 @@
 // The FMAs run as FFMA2 (two channels per instruction), and the
 // accumulator is initialised with the folded constant, so one output costs
 // 4.5 FFMA2 + 0.5 FMUL2 + 0.5 FADD2 on the FMA pipes and ~1.5 PRMT + FMNMX +
-// IADD + 0.5 I2IP on the integer pipe.
+// IADD + 0.5 I2IP on the integer pipe.  Measured on C4 it is register-operand
+// bound (83 us vs 71 us for the 64-channel tensor-core kernel, DESIGN.md
+// §4.4), so dispatch uses it where that kernel does not fit (W + 2 > 128).
 //
 // Layout: a CTA owns 128 channels (one 32-bit word = 4 channels per lane,
 // so every shared-memory word load of a warp is one conflict-free 128-byte
