@@ -383,6 +383,7 @@ constexpr int R2 = 2;       // output rows per unit, one 128-position M tile eac
 constexpr int NB2 = 4;      // halo buffers
 constexpr int KG = CB / 32; // K-groups of 32 channels
 constexpr int N2 = 64;      // MMA N: 32 outputs + 32 zero-point columns
+constexpr int EPI64 = 4 * R2 * KG;  // epilogue warps: (row, K-group) x TMEM lane quarter
 
 struct Dw2Layout {
     int halo_off, halo_stride, b_off, corr_off, mult_off, out_off, out_stride, bar_off, tmemptr_off, total;
@@ -415,7 +416,7 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
     return d;
 }
 
-__global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
+__global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     dwconv_tc64_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                        const DwParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -437,7 +438,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     const int c0 = cb * CB;
     ptx::griddep_launch_dependents();
 
-    if (warp == 0 && lane == 0) {
+    // roles: warps 0..EPI64-1 epilogue (TMEM lane quarter = warp % 4), then the
+    // halo producer, the TMEM allocator, an idle warp and the MMA issuer last:
+    // the warp scheduler favours the highest warp id, so the single-thread MMA
+    // issue loop is not starved by the ALU-heavy epilogue warps of its SMSP
+    constexpr int W_PROD = EPI64, W_ALLOC = EPI64 + 1, W_MMA = EPI64 + 3;
+    if (warp == W_PROD && lane == 0) {
         ptx::prefetch_tmap(&tmap_x);
         ptx::prefetch_tmap(&tmap_y);
         for (int b = 0; b < NB2; ++b) {
@@ -446,11 +452,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(tfull_bar(a), 1);
-            ptx::mbar_init(tempty_bar(a), EPI_WARPS);
+            ptx::mbar_init(tempty_bar(a), EPI64);
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
+    if (warp == W_ALLOC) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
     // (filter tables are immutable: built before griddepcontrol.wait, PDL)
 
     // ---- B for this channel block, per (tap, K-group): [K half][64 rows][16 B];
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     const uint32_t tmem_base = *tmem_ptr;
     const uint32_t halo_bytes = (uint32_t)((R2 + 2) * p.wp * CB);
 
-    if (warp == 0) {
+    if (warp == W_PROD) {
         // ------------------------------------------------ halo producer
         ptx::griddep_wait();  // x may be the previous grid's output
         int b = 0;
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 ph ^= 1;
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         // ------------------------------------------------ MMA issuer
         constexpr uint32_t idesc = ptx::idesc_u8s8_s32<128, N2>();
         // descriptors as uniform-register adds off two bases (an array of 36
@@ -547,13 +553,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 aph ^= 1;
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp < EPI64) {
         // ------------------------------------------------ requant epilogue
         ptx::griddep_wait();  // y may be read / written by the previous grid
-        // warpgroup r = output row r of the unit; thread = one position
-        const int ew = warp - 4, r = ew / 4, quarter = ew % 4;
+        // warp = (output row r, K-group j) of the unit x TMEM lane quarter
+        // (warp % 4); thread = one position.  16 warps (4 per SM sub-partition)
+        // keep the TMEM-load latency covered.
+        const int ew = warp, quarter = warp % 4, r = (ew / 4) / KG, j = (ew / 4) % KG;
         const int m = quarter * 32 + lane, ocol = m - 1;
-        const float magic = 12582912.0f;  // 1.5 * 2^23 (cterm carries its bit pattern)
+        const float2 magic2 = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23 (cterm carries its bit pattern)
+        const float2 nmagic2 = make_float2(-12582912.0f, -12582912.0f);
         const float floor_x = p.lo == 0.0f ? 0.0f : -8388608.0f;  // ReLU: 0; else -2^23 (see conv_tc.cu)
         const int32_t zoff = 0x4B400000 - p.zp_c;
         // the unit's 2 x W x 64 output bytes go to a shared-memory tile and out
@@ -570,50 +579,59 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             uint8_t* tile = smem + L.out_off + (ui & 1) * L.out_stride;
             // the store issued from this buffer two units ago has read it
             if (storer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI64) : "memory");
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
             if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
-            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + r * KG * N2);
+            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + (r * KG + j) * N2);
             const int q = r * p.w + ocol;  // 64-byte row of the tile (SWIZZLE_64B: chunk ^= (q >> 1) & 3)
+            // all 32 channels of this warp's tile out of TMEM first, then hand the
+            // accumulator buffer back to the MMA warp before the requant math
+            uint32_t vw[2][16], vz[2][16];
 #pragma unroll
-            for (int j = 0; j < KG; ++j) {
-                uint32_t vw[32], vz[32];
-                ptx::tmem_ld_32x32b_x32(lane_base + (uint32_t)(j * N2), vw);
-                ptx::tmem_ld_32x32b_x32(lane_base + (uint32_t)(j * N2 + 32), vz);
-                ptx::tmem_ld_wait();
-                const int4* cq = reinterpret_cast<const int4*>(corr_s + cls * CB + j * 32);
-                const float4* mq = reinterpret_cast<const float4*>(mult_s + j * 32);
-                uint32_t w8[8];
-#pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    const int4 cc = cq[g];
-                    const float4 mm = mq[g];
-                    const int32_t cv[4] = {cc.x, cc.y, cc.z, cc.w};
-                    const float mv[4] = {mm.x, mm.y, mm.z, mm.w};
-                    int32_t rr[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        // exact int -> float via the magic bits (|adj| < 2^22, checked at filter creation)
-                        const int32_t bits = (int32_t)(vw[4 * g + e] + vz[4 * g + e]) + cv[e];
-                        float x = __fmul_rn(__fsub_rn(__int_as_float(bits), magic), mv[e]);
-                        x = fmaxf(x, floor_x);
-                        rr[e] = __float_as_int(__fadd_rn(x, magic)) - zoff;
-                    }
-                    w8[g] = pack_sat_u8(rr[1], rr[0], pack_sat_u8(rr[3], rr[2], 0u));
-                }
-                if (ocol >= 0 && ocol < p.w) {
-                    uint4* row16 = reinterpret_cast<uint4*>(tile + (size_t)q * 64);
-                    row16[(2 * j) ^ ((q >> 1) & 3)] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
-                    row16[(2 * j + 1) ^ ((q >> 1) & 3)] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
-                }
+            for (int hh = 0; hh < 2; ++hh) {
+                ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(hh * 16), vw[hh]);
+                ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(32 + hh * 16), vz[hh]);
             }
-            (void)valid;
+            ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {  // 16 channels at a time
+                const int4* cq = reinterpret_cast<const int4*>(corr_s + cls * CB + j * 32 + hh * 16);
+                const float4* mq = reinterpret_cast<const float4*>(mult_s + j * 32 + hh * 16);
+                uint32_t w4[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int4 cc = cq[g];
+                    const float4 mm = mq[g];
+                    // exact int -> float via the magic bits (|adj| < 2^22, checked at filter creation)
+                    const int32_t b0 = (int32_t)(vw[hh][4 * g] + vz[hh][4 * g]) + cc.x;
+                    const int32_t b1 = (int32_t)(vw[hh][4 * g + 1] + vz[hh][4 * g + 1]) + cc.y;
+                    const int32_t b2 = (int32_t)(vw[hh][4 * g + 2] + vz[hh][4 * g + 2]) + cc.z;
+                    const int32_t b3 = (int32_t)(vw[hh][4 * g + 3] + vz[hh][4 * g + 3]) + cc.w;
+                    float2 x01 = __fmul2_rn(__fadd2_rn(make_float2(__int_as_float(b0), __int_as_float(b1)), nmagic2),
+                                            make_float2(mm.x, mm.y));
+                    float2 x23 = __fmul2_rn(__fadd2_rn(make_float2(__int_as_float(b2), __int_as_float(b3)), nmagic2),
+                                            make_float2(mm.z, mm.w));
+                    x01.x = fmaxf(x01.x, floor_x);
+                    x01.y = fmaxf(x01.y, floor_x);
+                    x23.x = fmaxf(x23.x, floor_x);
+                    x23.y = fmaxf(x23.y, floor_x);
+                    x01 = __fadd2_rn(x01, magic2);
+                    x23 = __fadd2_rn(x23, magic2);
+                    w4[g] = pack_sat_u8(__float_as_int(x01.y) - zoff, __float_as_int(x01.x) - zoff,
+                                        pack_sat_u8(__float_as_int(x23.y) - zoff, __float_as_int(x23.x) - zoff, 0u));
+                }
+                if (ocol >= 0 && ocol < p.w) {
+                    uint4* row16 = reinterpret_cast<uint4*>(tile + (size_t)q * 64);
+                    row16[(2 * j + hh) ^ ((q >> 1) & 3)] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
+            }
+            (void)valid;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile writes -> TMA
-            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI64) : "memory");
             if (storer) {
                 // rows past H are clipped by the tensor map
                 asm volatile(
@@ -635,7 +653,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     __syncwarp();
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == W_ALLOC) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem_base);
     }
@@ -719,7 +737,7 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
         int per_blk = sm_count(dev) / p.nblk;
         if (per_blk < 1) per_blk = 1;
         if (per_blk > p.units_blk) per_blk = p.units_blk;
-        const cudaError_t e = launch_with_pdl(dwconv_tc64_kernel, dim3(per_blk * p.nblk), dim3(128 + 32 * EPI_WARPS),
+        const cudaError_t e = launch_with_pdl(dwconv_tc64_kernel, dim3(per_blk * p.nblk), dim3(128 + 32 * EPI64),
                                               dw2_layout(p.wp).total, s, tmap, tmap_y, p);
         count_launch(kFamDwTc);
         return e;
