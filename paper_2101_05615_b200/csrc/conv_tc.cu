@@ -219,6 +219,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
     const CvLayout L = cv_layout(p);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // roles: warps 0..EPI_WARPS-1 epilogue (TMEM lane quarter = warp % 4), then
+    // the halo producer, MMA issuer 0 (SMSP 1), the TMEM allocator and MMA
+    // issuer 1 (SMSP 3): the scheduler favours the highest warp id, so the
+    // issue loops are not starved by the ALU-heavy epilogue warps
+    constexpr int W_PROD = EPI_WARPS, W_MMA0 = EPI_WARPS + 1, W_ALLOC = EPI_WARPS + 2, W_MMA1 = EPI_WARPS + 3;
     const uint32_t bar0 = base + L.bar_off;
     auto full_bar = [&](int b) { return bar0 + 8u * b; };
     auto empty_bar = [&](int b) { return bar0 + 8u * (MAX_BUF + b); };
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) cv_pstamp(p, 1);
-    if (warp == 2) {
+    if (warp == W_ALLOC) {
         ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
         if (lane == 0) cv_pstamp(p, 2);
     }
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         p.trace[8192 + 320] = t;
     }
 
-    if (warp == 0) {
+    if (warp == W_PROD) {
         // ------------------------------------------------ halo producer
         ptx::griddep_wait();
         if (!p.img_prefetch && ptx::elect_one()) {  // image built by this call's conv_prep_kernel
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 ph ^= 1;
             }
         }
-    } else if (warp == 1 || warp == 3) {
+    } else if (warp == W_MMA0 || warp == W_MMA1) {
         // ------------------------------------------------ MMA issuer
         // The whole warp runs the loop (warp-uniform control flow) and one
         // elected lane issues: every descriptor is then a uniform-register
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         // each shares its SMSP with an epilogue warp, and a busy neighbour
         // delays a warp's next issue (tools/mma_desc.cu); with two, one of
         // them usually has the next unit's MMAs queued
-        const int q = warp == 1 ? 0 : 1;
+        const int q = warp == W_MMA0 ? 0 : 1;
         ptx::mbar_wait(img_bar, 0);
         int ui = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
@@ -356,10 +361,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             }
             __syncwarp();
         }
-    } else if (warp >= 4) {
+    } else if (warp < EPI_WARPS) {
         // ------------------------------------------------ epilogue
         // warpgroup wg (warps 4-7 / 8-11) owns TMEM buffer wg = every other unit
-        const int wg = (warp - 4) / 4;
+        const int wg = warp / 4;
         const int quarter = warp % 4;
         const int r = quarter * 32 + lane;  // position within the unit's tile
         const int orow = r / p.wp, ocol = r % p.wp - 1;
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         {
             // per-CTA tables: corr[class][n] = c[n] + zp_a * sum over the
             // class's padded taps of (tap weight sum - C*zp_b[n]); SoA copies
-            const int et = threadIdx.x - 128;
+            const int et = threadIdx.x;
             ptx::mbar_wait(img_bar, 0);
             const int32_t* wsum = reinterpret_cast<const int32_t*>(smem + L.wsum_off);
             int32_t* corr_w = reinterpret_cast<int32_t*>(smem + L.corr_off);
@@ -499,7 +504,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     __syncwarp();
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == W_ALLOC) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem_base);
     }
