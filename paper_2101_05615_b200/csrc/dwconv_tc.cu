@@ -404,6 +404,15 @@ __host__ __device__ inline Dw2Layout dw2_layout(int wp) {
     return L;
 }
 
+// zero 16 TMEM columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_st_zero16(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(z)
+        : "memory");
+}
+
 __host__ __device__ inline uint64_t kmajor_swz64_desc(uint32_t addr) {
     return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)4 << 61);  // SWIZZLE_64B, 8-row groups of 512 B
@@ -459,15 +468,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     if (warp == W_ALLOC) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
     // (filter tables are immutable: built before griddepcontrol.wait, PDL)
 
-    // ---- B for this channel block, per (tap, K-group): [K half][64 rows][16 B];
-    // row n < 32: w[t][c0 + 32j + n] at K index n; row 32 + n: -zp_w at K index n
-    for (int idx = threadIdx.x; idx < 9 * KG * 128; idx += blockDim.x) {
-        const int t = idx / (KG * 128), rem = idx % (KG * 128);
-        const int j = rem / 128, half = (rem % 128) / 64, n = rem % 64;
-        const int oc = n % 32, ch = c0 + j * 32 + oc;
+    // ---- B for this channel block, per (kw, K-group): [K half][192 rows][16 B],
+    // rows [64 kh, 64 kh + 32): w[kh*3 + kw][c0 + 32j + n] at K index n, rows
+    // [64 kh + 32, 64 kh + 64): -zp_w at K index n.  One MMA over an input row
+    // then feeds two output rows: its N columns are [W_kh | Z | W_kh+1 | Z]
+    // and land in two adjacent TMEM row slots (see the MMA issuer).
+    for (int idx = threadIdx.x; idx < 3 * KG * 2 * 192; idx += blockDim.x) {
+        const int kw = idx / (KG * 384), rem = idx % (KG * 384);
+        const int j = rem / 384, half = (rem % 384) / 192, n = rem % 192;
+        const int kh = n / 64, wi = n % 64, oc = wi % 32, ch = c0 + j * 32 + oc;
         uint32_t v[4] = {0, 0, 0, 0};
         if (oc / 16 == half) {
-            const uint32_t byte = n < 32 ? (uint32_t)(uint8_t)p.wt[t * p.c + ch] : (uint32_t)(uint8_t)(int8_t)(-p.zpw[ch]);
+            const uint32_t byte = wi < 32 ? (uint32_t)(uint8_t)p.wt[(kh * 3 + kw) * p.c + ch]
+                                          : (uint32_t)(uint8_t)(int8_t)(-p.zpw[ch]);
             v[(oc % 16) / 4] = byte << (8 * (oc % 4));
         }
         *reinterpret_cast<uint4*>(smem + L.b_off + (size_t)idx * 16) = make_uint4(v[0], v[1], v[2], v[3]);
@@ -489,6 +502,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_ptr;
     const uint32_t halo_bytes = (uint32_t)((R2 + 2) * p.wp * CB);
+    // TMEM per accumulator buffer: [K-group j][slot 0: output row r0 + 1 | slot 1: row r0] x 64
+    // columns (32 sum x*w, 32 -zp_w * sum x).  Slot 0 is first written by an
+    // accumulating MMA, so it starts zeroed and the epilogue re-zeroes it after reading.
+    if (warp < EPI64 && (warp / 4) / KG == 1) {
+        const uint32_t zb = tmem_base + ((uint32_t)((warp % 4) * 32) << 16) + (uint32_t)(((warp / 4) % KG) * 128);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) tmem_st_zero16(zb + (uint32_t)(a * 256 + q4 * 16));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
 
     if (warp == W_PROD) {
         // ------------------------------------------------ halo producer
@@ -512,14 +539,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         }
     } else if (warp == W_MMA) {
         // ------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = ptx::idesc_u8s8_s32<128, N2>();
-        // descriptors as uniform-register adds off two bases (an array of 36
-        // precomputed descriptors spilled out of the uniform registers and
-        // slowed the issue): tile r, tap t starts at halo position
-        // (r + t/3)*(W+2) + t%3 - 1 (the +1 shift keeps fields >= 0)
+        constexpr uint32_t idesc64 = ptx::idesc_u8s8_s32<128, 64>();
+        constexpr uint32_t idesc128 = ptx::idesc_u8s8_s32<128, 128>();
         const uint64_t a0 = kmajor_swz64_desc(0u);
         const uint64_t row16 = (uint64_t)(p.wp * CB / 16), pos16 = CB / 16;
-        const uint64_t b0 = kmajor_noswz_desc(base + L.b_off, 1024, 128);
+        const uint64_t b0 = kmajor_noswz_desc(base + L.b_off, 192 * 16, 128);
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas) {
@@ -529,16 +553,26 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride - (uint32_t)CB) >> 4);
             if (ptx::elect_one()) {
                 dw_stamp(p, 1, (k - cta_in) / ctas);
+                // halo row i = input row r0 - 1 + i feeds output row r0 + 1 with
+                // tap row kh = i - 1 and output row r0 with kh = i:
+                //   i = 0: r0 (kh 0)               N = 64 into slot 1
+                //   i = 1: r0+1 (kh 0), r0 (kh 1)  N = 128 into slots 0-1
+                //   i = 2: r0+1 (kh 1), r0 (kh 2)  N = 128 into slots 0-1
+                //   i = 3: r0+1 (kh 2)             N = 64 into slot 0
 #pragma unroll
-                for (int r = 0; r < R2; ++r)
+                for (int i = 0; i < R2 + 2; ++i)
 #pragma unroll
-                    for (int j = 0; j < KG; ++j) {
-                        const uint32_t d = tmem_base + (uint32_t)(acc * 256 + (r * KG + j) * N2);
+                    for (int kw = 0; kw < 3; ++kw)
 #pragma unroll
-                        for (int t = 0; t < 9; ++t)
-                            ptx::mma_i8(d, ahalo + (uint64_t)(r + t / 3) * row16 + (uint64_t)(t % 3) * pos16 + 2u * j,
-                                        b0 + (uint64_t)((t * KG + j) * 128), idesc, t != 0);
-                    }
+                        for (int j = 0; j < KG; ++j) {
+                            const uint64_t ad = ahalo + (uint64_t)i * row16 + (uint64_t)kw * pos16 + 2u * j;
+                            const uint64_t bd = b0 + (uint64_t)((kw * KG + j) * 384);
+                            const uint32_t d = tmem_base + (uint32_t)(acc * 256 + j * 128);
+                            if (i == 0) ptx::mma_i8(d + 64, ad, bd, idesc64, kw != 0);
+                            if (i == 1) ptx::mma_i8(d, ad, bd, idesc128, 1);
+                            if (i == 2) ptx::mma_i8(d, ad, bd + 64, idesc128, 1);
+                            if (i == 3) ptx::mma_i8(d, ad, bd + 128, idesc64, 1);
+                        }
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
                 dw_stamp(p, 2, (k - cta_in) / ctas);
@@ -583,7 +617,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
             if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
-            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + (r * KG + j) * N2);
+            const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + j * 128 + (1 - r) * 64);
             const int q = r * p.w + ocol;  // 64-byte row of the tile (SWIZZLE_64B: chunk ^= (q >> 1) & 3)
             // all 32 channels of this warp's tile out of TMEM first, then hand the
             // accumulator buffer back to the MMA warp before the requant math
@@ -594,6 +628,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(32 + hh * 16), vz[hh]);
             }
             ptx::tmem_ld_wait();
+            if (r == 1) {  // slot 0 must be zero before the accumulating MMAs of the buffer's next unit
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) tmem_st_zero16(lane_base + (uint32_t)(q4 * 16));
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
