@@ -1,6 +1,9 @@
 """Benchmark of the B200 fused u8 x s8 -> s32 GEMM + requantization hot path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C0|C1|C2|C3|C4] [--impl ours|reference]
+
+(C3 / C4: conv 3x3 and depthwise 3x3 with the batch sharded over ranks; the
+default, the headline, is C1.)
 
 One JSON line on rank 0.  A "step" is one pass of the hot path over one batch:
 one fused GEMM + per-channel requant + ReLU launch at BASELINE configs[1]
@@ -52,6 +55,13 @@ CONFIGS = {
                                    "(BASELINE configs[2])"),
     "C0": (64, 800, 320, 0.5, "C0 single FC: M=64 N=800 K=320 (BASELINE configs[0], F32_RNE)"),
 }
+# conv workloads (batch sharded over ranks): name -> (images/GPU, H, W, C, OC or 0 = depthwise, alpha_C, description)
+CONV_CONFIGS = {
+    "C3": (32, 56, 56, 64, 64, 0.8, "C3 conv3x3 as implicit GEMM: NHWC 32x56x56x64 -> 64, pad 1 with zp_a, "
+                                    "per-channel requant + ReLU (BASELINE configs[3])"),
+    "C4": (32, 112, 112, 256, 0, 0.1, "C4 depthwise 3x3: NHWC 32x112x112x256, pad 1 with zp_a, per-channel "
+                                      "requant + ReLU (BASELINE configs[4])"),
+}
 
 
 def peaks():
@@ -74,7 +84,7 @@ def int8_peaks():
 
 # roofline bound per config: C0 launch-latency (reported
 # against HBM), C1 HBM (intensity 240 < ridge), C2 tensor
-BOUND = {"C0": "hbm", "C1": "hbm", "C2": "tensor"}
+BOUND = {"C0": "hbm", "C1": "hbm", "C2": "tensor", "C3": "hbm", "C4": "hbm"}
 
 
 def max_over_ranks(vals, device, world):
@@ -195,11 +205,84 @@ def cpu_reference(cfg: str, steps: int, warmup: int, threads: int, budget_s: flo
             "ms_per_step": sec * 1e3, "steps_timed": len(times)}
 
 
+def conv_ops_bytes(cfg: str, nb: int):
+    """Algorithmic int8 ops and bytes of one conv / depthwise launch over nb images
+    (x + y + weights + per-channel tables)."""
+    _, h, w, c, oc, _, _ = CONV_CONFIGS[cfg]
+    if oc:
+        return 2.0 * nb * h * w * oc * 9 * c, nb * h * w * (c + oc) + 9 * c * oc + 16 * oc
+    return 2.0 * 9 * nb * h * w * c, 2 * nb * h * w * c + 9 * c + 16 * c
+
+
+def conv_inputs(cfg: str):
+    """Weights and per-channel requant parameters (BASELINE distributions, App. A D4)."""
+    _, h, w, c, oc, alpha_c, _ = CONV_CONFIGS[cfg]
+    r = np.random.default_rng(11)
+    nout = oc or c
+    wt = r.integers(-128, 128, (3, 3, c, oc) if oc else (3, 3, c)).astype(np.int8)
+    bias = r.integers(-1000, 1001, nout).astype(np.int32)
+    zp_b = r.integers(-10, 11, nout).astype(np.int32)
+    mult = (0.02 * r.uniform(0.005, 0.02, nout) / alpha_c).astype(np.float32)
+    return wt, bias, zp_b, mult
+
+
+def cpu_reference_conv(cfg: str, threads: int, budget_s: float = 15.0, images: int = 0):
+    """C3: restated im2col + the reference execute_gemm (oracle/_ref) + restated
+    per-channel requant; C4: the restated depthwise loop (no reference path),
+    on a bounded sample of images of the workload."""
+    from oracle.py import Oracle, RefLib  # CPU baseline leg only
+    _, h, w, c, oc, _, _ = CONV_CONFIGS[cfg]
+    orc = Oracle()
+    wt, bias, zp_b, mult = conv_inputs(cfg)
+    nimg = images or (2 if oc else 1)
+    x = np.random.default_rng(5).integers(0, 256, (nimg, h, w, c)).astype(np.uint8)
+    if oc:
+        ref = RefLib()
+        wk = wt.reshape(9 * c, oc)
+        pk = ref.prepack(wk, ref.select_blocking(nimg * h * w, oc, 9 * c))
+        colsum = pk.col_offsets()
+
+        def step():
+            cols = orc.im2col3x3(x, 128, threads=threads)
+            acc = pk.gemm_raw(cols, threads=threads)
+            return orc.requant_matrix(acc, orc.row_offsets(cols), colsum, 128, zp_b, 9 * c, bias, 1, mult, 5, True,
+                                      per_channel=True)
+        kind, what = "reference", "restated im2col + reference execute_gemm[WriteRawI32] + restated requant"
+    else:
+        def step():
+            return orc.dwconv3x3(x, 128, wt, zp_b, bias, mult, 5, True, threads=threads)
+        kind, what = "port", "restated depthwise loop (the reference has no depthwise path)"
+    step()
+    times = []
+    t_all = time.perf_counter()
+    while not times or (time.perf_counter() - t_all < budget_s and len(times) < 20):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    sec = float(np.median(times))
+    ops, _ = conv_ops_bytes(cfg, nimg)
+    return {"value": ops / sec / 1e12, "unit": "TOPS", "cores": threads, "kind": kind,
+            "sample": f"{nimg} of the workload's images, {what}, median of {len(times)}, {threads} threads",
+            "ms_per_step": sec * 1e3 * CONV_CONFIGS[cfg][0] / nimg, "steps_timed": len(times)}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
+    if args.config in CONV_CONFIGS:
+        res = cpu_reference_conv(args.config, threads, budget_s=min(120.0, 5.0 + 2.0 * args.steps))
+        desc = CONV_CONFIGS[args.config][-1]
+        line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "TOPS", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
+                "data": "synthetic (seeded numpy RNG, BASELINE distributions)",
+                "config": {"workload": desc, "path": "CPU " + res["kind"] + " (oracle/)"},
+                "cpu_baseline": {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": res["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
     res = cpu_reference(args.config, args.steps, args.warmup, threads)
     m, n, k, _, desc = CONFIGS[args.config]
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "TOPS", "n_gpus": args.gpus,
@@ -404,12 +487,174 @@ def run_ours(args):
     return 0
 
 
+def run_conv_ours(args):
+    """C3 / C4: each rank convolves its own batch of images (batch sharded, no
+    collective); same timing rules as the GEMM arm."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2101_05615_b200 as q8
+    from paper_2101_05615_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", local if world > 1 else 0)
+    didx = dev.index
+    nb, h, w, c, oc, _, desc = CONV_CONFIGS[args.config]
+    nout = oc or c
+    wt, bias, zp_b, mult = conv_inputs(args.config)
+    rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=9 * c if oc else 9, bias=bias, zp_b_per_channel=zp_b,
+                          multiplier_f32_per_channel=mult, rounding=q8.ROUND_F32_RNE)
+    if oc:
+        pw = q8.prepack_conv3x3_weights(wt, device=didx)
+        pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
+
+        def call(x, y):
+            q8.execute_conv3x3(x, pw, y, pipe)
+    else:
+        filt = q8.DepthwiseFilter(wt, rp, relu=True, device=didx)
+
+        def call(x, y):
+            q8.execute_dwconv3x3(x, filt, y)
+    ops, abytes = conv_ops_bytes(args.config, nb)
+    set_bytes = nb * h * w * (c + nout)
+    nsets = max(2, min(64, int(np.ceil(2.2 * 126e6 / set_bytes))))
+    g = torch.Generator(device=dev)
+    g.manual_seed(99 + rank)
+    xs = [torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device=dev, generator=g) for _ in range(nsets)]
+    ys = [torch.empty((nb, h, w, nout), dtype=torch.uint8, device=dev) for _ in range(nsets)]
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    def launch(i):
+        call(xs[i % nsets], ys[i % nsets])
+
+    for i in range(max(args.warmup, nsets)):
+        launch(i)
+    torch.cuda.synchronize(dev)
+    c0 = _lib.launch_count()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for i in range(args.steps):
+            launch(i)
+    launches_per_step = (_lib.launch_count() - c0) / args.steps
+    ev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+          for _ in range(nsets)]
+    graph_ev = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_ev, stream=stream):
+        for i in range(nsets):
+            ev[i][0].record(stream)
+            launch(i)
+            ev[i][1].record(stream)
+    graph_ev.replay()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(didx)
+    sampler.start()
+    time.sleep(0.3)
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        graph_ev.replay()
+        torch.cuda.synchronize(dev)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    start.record(stream)
+    graph.replay()
+    end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    clocks = sampler.stop()
+    kern_ms = []
+    for _ in range(3):
+        graph_ev.replay()
+        torch.cuda.synchronize(dev)
+        kern_ms += [a.elapsed_time(bb) for a, bb in ev]
+    kern_ms = float(np.mean(kern_ms))
+
+    # e2e through the public API: pinned x -> device, the call, y -> pinned host, every step
+    x_host = torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, generator=torch.Generator().manual_seed(4))
+    x_host = x_host.pin_memory()
+    y_host = torch.empty((nb, h, w, nout), dtype=torch.uint8).pin_memory()
+    e2e_steps = max(1, min(args.steps, 20))
+
+    def e2e_call():
+        xs[0].copy_(x_host, non_blocking=True)
+        call(xs[0], ys[0])
+        y_host.copy_(ys[0], non_blocking=True)
+
+    for _ in range(2):
+        e2e_call()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_call()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_s = e0.elapsed_time(e1) * 1e-3 / e2e_steps
+    if world > 1:
+        dist.barrier()
+    ms, kern_ms, e2e_s = max_over_ranks([ms, kern_ms, e2e_s], dev, world)
+    if rank == 0:
+        ms_step = ms / args.steps
+        kern_avg_ms = ms_step / max(1.0, launches_per_step)
+        hbm, _, src = peaks()
+        achieved = abytes / (kern_avg_ms * 1e-3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get(args.config)
+        line = {
+            "metric": METRIC, "value": ops * world / (ms_step * 1e-3) / 1e12, "unit": "TOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
+            "data": "synthetic (seeded torch / numpy RNG, BASELINE distributions)",
+            "config": {"workload": desc, "images_per_gpu": nb, "global_images": nb * world,
+                       "parallelism": f"batch sharded x{world}, weights replicated, no collective",
+                       "l2": f"{nsets} rotating buffer sets, {nsets * set_bytes / 1e6:.0f} MB > 2x126 MB L2",
+                       "graph": "K steps captured in one CUDA graph", "packing": "excluded (prepacked once)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "peak_source": src + " (MEASURED_PEAKS.json hbm_gbs)", "traffic": traffic,
+                         "algorithmic_bytes_per_launch": abytes, "kernel_ms": kern_avg_ms,
+                         "kernel_ms_isolated": kern_ms, "int8_tops_per_launch": ops / (kern_avg_ms * 1e-3) / 1e12},
+            "e2e": {"value": ops * world / e2e_s / 1e12, "unit": "TOPS",
+                    "h2d_bytes_per_step": nb * h * w * c * world, "d2h_bytes_per_step": nb * h * w * nout * world,
+                    "ms_per_step": e2e_s * 1e3, "path": "pinned x -> device, execute_conv3x3 / execute_dwconv3x3, "
+                                                        "y -> pinned host"},
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cb = cpu_reference_conv(args.config, os.cpu_count() or 1)
+                line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:  # the baseline is reported, never the target
+                line["cpu_baseline"] = {"value": None, "unit": "TOPS", "cores": 0, "kind": "port",
+                                        "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS) + sorted(CONV_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -417,6 +662,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.config in CONV_CONFIGS:
+        return run_conv_ours(args)
     return run_ours(args)
 
 
