@@ -1,0 +1,43 @@
+"""bench.py's reference arm (CPU, no GPU needed): one JSON line with the
+driver's contract keys for the GEMM headline and the conv / depthwise
+workloads, and silent non-zero ranks under torchrun."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def run_bench(*args, env_extra=None, timeout=300):
+    env = dict(os.environ)
+    env.update(env_extra or {})
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True, cwd=ROOT,
+                       env=env, timeout=timeout)
+    return r.returncode, r.stdout, r.stderr
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3", "C4"])
+def test_reference_arm_line(cfg):
+    if not (ROOT / "oracle" / "_ref").exists() and cfg != "C4":
+        pytest.skip("oracle/_ref not built")
+    rc, out, err = run_bench("--impl", "reference", "--config", cfg, "--steps", "1", "--warmup", "3")
+    assert rc == 0, err
+    lines = [ln for ln in out.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "TOPS" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["e2e"]["value"] == d["value"] == d["cpu_baseline"]["value"]
+    assert d["cpu_baseline"]["kind"] == ("port" if cfg == "C4" else "reference")
+    assert d["cpu_baseline"]["cores"] >= 1
+
+
+def test_reference_arm_other_ranks_silent():
+    rc, out, _ = run_bench("--impl", "reference", "--config", "C1", "--steps", "1", "--gpus", "2",
+                           env_extra={"RANK": "1", "WORLD_SIZE": "2"})
+    assert rc == 0 and out.strip() == ""
