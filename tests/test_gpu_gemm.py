@@ -432,3 +432,35 @@ def test_requant_fuzz_vs_oracle(cuda, orc, seed):
                              mult if per_channel else mult, zp_c, relu, per_channel=per_channel)
     got = out.cpu().numpy()
     assert (got == exp).all(), (m, n, k, per_channel, relu, rounding, int((got != exp).sum()))
+
+
+# host-view entry with pageable and pinned output buffers: a wide ldc and a
+# row stripe leave everything outside the stripe untouched, and both give
+# the same bytes
+@pytest.mark.parametrize("shape", [(128, 4096, 4096), (130, 256, 200), (1, 64, 48)])
+def test_host_path_pinned_and_pageable_output(cuda, orc, shape):
+    from paper_2101_05615_b200 import _lib
+    m, n, k = shape
+    c = configs.gemm_case(orc, "C1", m, n, k, seed=sum(shape))
+    pw = q8.prepack_weights(c.b)
+    pipe = requant_pipeline(c, k, q8.ROUND_F32_RNE)  # owns the epilogue handle
+    ep = pipe.epilogue(pw)
+    lib = _lib.load()
+    a = np.ascontiguousarray(c.a)
+    ldc = n + 16
+    r0 = 1 if m > 1 else 0
+    staged = np.full((m, ldc), 7, np.uint8)
+    _lib.check(lib.q8g_gemm_u8s8_requant_host(a.ctypes.data, m, k, k, pw.handle, ep, staged.ctypes.data, ldc, r0, m,
+                                              None))
+    pinned = torch.full((m, ldc), 7, dtype=torch.uint8).pin_memory()
+    _lib.check(lib.q8g_gemm_u8s8_requant_host(a.ctypes.data, m, k, k, pw.handle, ep, pinned.data_ptr(), ldc, r0, m,
+                                              None))
+    assert (pinned.numpy() == staged).all()
+    assert (pinned.numpy()[:r0] == 7).all() and (pinned.numpy()[:, n:] == 7).all()
+    raw = torch.full((m, ldc), -5, dtype=torch.int32).pin_memory()
+    _lib.check(lib.q8g_gemm_u8s8_raw_i32_host(a.ctypes.data, m, k, k, pw.handle, raw.data_ptr(), ldc, r0, m, None))
+    exp = orc.naive_gemm_i32(a[r0:], c.b) if m * n * k <= 1 << 24 else None
+    got = raw.numpy()
+    if exp is not None:
+        assert (got[r0:, :n] == exp).all()
+    assert (got[:r0] == -5).all() and (got[:, n:] == -5).all()
