@@ -104,6 +104,18 @@ __device__ __forceinline__ void t2_kb(const Tc2Params& p, int which, int kb) {
     }
 }
 
+// CTA 0: SM clock and globaltimer at kernel entry / exit (effective SM clock
+// of the launch, tools/c2_clock.py): [10200] clock0 [10201] clock1 [10202] t0 [10203] t1
+__device__ __forceinline__ void t2_clk(const Tc2Params& p, int end) {
+    if (p.trace && blockIdx.x == 0) {
+        unsigned long long t, c;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+        p.trace[10200 + end] = c;
+        p.trace[10202 + end] = t;
+    }
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -124,6 +136,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) t2_stamp(p, 0);
+    if (threadIdx.x == 0) t2_clk(p, 0);
     const uint32_t rank = ptx::cluster_ctarank();
     const uint32_t lrank = rank & ~1u;         // this CTA's pair leader
     const bool leader = (rank & 1u) == 0;
@@ -369,6 +382,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     __syncthreads();
     cluster_sync_all();  // the pair finishes together before TMEM is released
     if (threadIdx.x == 0) t2_stamp(p, 7);
+    if (threadIdx.x == 0) t2_clk(p, 1);
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc_pair<512>(tmem_base);

@@ -213,6 +213,8 @@ cudaError_t launch_post(int writer, const int32_t* acc, int ldacc, const uint8_t
                         const q8g_sparse_csc* sp, const q8g_epilogue* ep, double dq_scale, int32_t dq_zp, void* out,
                         int ldc, cudaStream_t s);
 cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s);
+bool tc2w_supported(const GemmArgs& g);
+cudaError_t launch_gemm_tc2w(const GemmArgs& g, cudaStream_t s);
 int tc_trace_copy(unsigned long long* out, int max_ctas);
 
 struct ConvArgs {

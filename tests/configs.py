@@ -9,6 +9,7 @@ chosen per config so the pre-clamp output spread is ~40 quanta.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from dataclasses import replace as dataclasses_replace  # noqa: F401 (tests)
 
 import numpy as np
 

@@ -351,16 +351,71 @@ def test_large_m_pair_kernel_repeated_runs_exact(cuda, orc):
     assert q8.launch_stats()["gemm_tc_large_m"] == before + 21
 
 
-def test_c2_full_size_row_subset_vs_oracle(cuda, orc):
-    """C2 at its full size (16384 x 4096 x 4096, the CTA-pair kernel): raw int32
-    and F32_RNE per-channel requant checked against the oracle on a row subset
-    covering tile / pair / stripe boundaries (the full naive
-    product would take minutes); two-stripe composition bit-identical."""
-    import dataclasses
+@pytest.mark.parametrize("m,n,k,ldc_pad", [(2500, 2000, 1008, 48), (5000, 1000, 512, 0), (2560, 2048, 1024, 1),
+                                           (2600, 4000, 256, 16)])
+@pytest.mark.parametrize("mode", ["raw", "f32", "f32_slow", "ref"])
+def test_wide_pair_kernel_ragged_shapes(cuda, orc, m, n, k, ldc_pad, mode):
+    """The 256 x 512 CTA-pair kernel (gemm_tc2w.cu) on ragged M / N (TMA-store
+    clipping), K not a multiple of 128, wide / unaligned output leading
+    dimensions (TMA store vs direct stores), every epilogue: raw int32,
+    F32_RNE fast (zp_c in [0,255]) and general (zp_c outside), REF."""
+    assert configs.tile_class(m, n) == 2 and (-(-n // 256) * 256) % 512 == 0
+    c = configs.gemm_case(orc, "C1", m, n, k, seed=m + n)
+    pw = q8.prepack_weights(c.b)
+    acc = orc.naive_gemm_i32(c.a, c.b)
+    ldc = n + ldc_pad
+    before = q8.launch_stats()["gemm_tc_large_m"]
+    if mode == "raw":
+        buf = torch.full((m, ldc), -7, dtype=torch.int32, device="cuda")
+        q8.execute_gemm(dev(c.a), pw, buf[:, :n], q8.OutputPipeline([q8.WriteRawI32()]))
+        torch.cuda.synchronize()
+        got = buf.cpu().numpy()
+        assert (got[:, :n] == acc).all()
+        assert (got[:, n:] == -7).all()
+    else:
+        rounding = q8.ROUND_REF if mode == "ref" else q8.ROUND_F32_RNE
+        if mode == "ref":
+            c = configs.dataclasses_replace(c, per_channel=False, zp_b=np.array(3, np.int32), mult_f64=3e-6)
+        if mode == "f32_slow":
+            c = configs.dataclasses_replace(c, zp_c=-300)  # not fast_f32: the general requant path
+        pipe = requant_pipeline(c, k, rounding)
+        exp = oracle_requant(orc, c, acc, rounding)
+        buf = torch.full((m, ldc), 0xA5, dtype=torch.uint8, device="cuda")
+        q8.execute_gemm(dev(c.a), pw, buf[:, :n], pipe)
+        torch.cuda.synchronize()
+        got = buf.cpu().numpy()
+        bad = np.argwhere(got[:, :n] != exp)
+        assert bad.size == 0, f"{len(bad)} mismatches, first {bad[:4].tolist()}"
+        assert (got[:, n:] == 0xA5).all()
+    assert q8.launch_stats()["gemm_tc_large_m"] == before + 1
+
+
+def _c2_reference_accumulators(orc, a, b):
+    """All 67 M int32 accumulators of C2 on the host: the unmodified reference
+    execute_gemm[WriteRawI32] (oracle/_ref) on every host core -- pinned to
+    oracle::naive_gemm_i32 by acceptance criterion 1 and test_oracle_kat --
+    or, where the reference library was not built, the oracle's naive GEMM."""
+    import os
+    try:
+        from oracle.py import RefLib
+        ref = RefLib()
+    except Exception:  # noqa: BLE001 - no oracle/_ref on this box
+        return orc.naive_gemm_i32(a, b, threads=os.cpu_count() or 1)
+    m, k = a.shape
+    pk = ref.prepack(b, ref.select_blocking(m, b.shape[1], k))
+    return pk.gemm_raw(a, threads=os.cpu_count() or 1)
+
+
+def test_c2_full_size_all_outputs_vs_reference(cuda, orc):
+    """C2 at its full size (16384 x 4096 x 4096, the 256 x 512 CTA-pair kernel):
+    EVERY raw int32 accumulator and EVERY per-channel F32_RNE requantized u8
+    output equals the reference's (acceptance.cpp:106-152 compares whole
+    matrices); a two-stripe composition is bit-identical."""
     m, n, k = configs.CONFIG_SHAPES["C2"]
     c = configs.gemm_case(orc, "C2", m, n, k, seed=2)
     pw = q8.prepack_weights(c.b)
     ad = dev(c.a)
+    before = q8.launch_stats()["gemm_tc_large_m"]
     raw = torch.zeros((m, n), dtype=torch.int32, device="cuda")
     q8.execute_gemm(ad, pw, raw, q8.OutputPipeline([q8.WriteRawI32()]))
     out = torch.zeros((m, n), dtype=torch.uint8, device="cuda")
@@ -370,21 +425,18 @@ def test_c2_full_size_row_subset_vs_oracle(cuda, orc):
     for t in (1, 0):
         q8.execute_gemm(ad, pw, out2, pipe, thread_id=t, num_threads=2)
     torch.cuda.synchronize()
+    assert q8.launch_stats()["gemm_tc_large_m"] == before + 4
     assert torch.equal(out, out2)
-    edges = [0, 1, 127, 128, 255, 256, 257, 8191, 8192, 8193, m - 257, m - 256, m - 129, m - 128, m - 1]
-    rows = np.array(sorted(set(edges) | set(np.random.default_rng(5).integers(0, m, 40).tolist())))
-    sub = dataclasses.replace(c, a=np.ascontiguousarray(c.a[rows]))
-    acc = orc.naive_gemm_i32(sub.a, c.b)
-    assert (raw[torch.from_numpy(rows).cuda()].cpu().numpy() == acc).all()
-    exp = oracle_requant(orc, sub, acc, 1)
-    assert (out[torch.from_numpy(rows).cuda()].cpu().numpy() == exp).all()
-    # size-independent property over all 67 M outputs: the raw accumulators'
-    # column sums equal the exact A-row-sum-weighted column sums of B
-    colsum_gpu = raw.to(torch.int64).sum(dim=0).cpu().numpy()
-    rs = c.a.astype(np.int64).sum(axis=0)  # sum over rows of A, per k
-    colsum_exact = rs @ c.b.astype(np.int64)
-    # raw int32 accumulators are exact (|acc| < 2^31 at K = 4096)
-    assert (colsum_gpu == colsum_exact).all()
+    acc = _c2_reference_accumulators(orc, c.a, c.b)
+    raw_h = raw.cpu().numpy()
+    bad = np.argwhere(raw_h != acc)
+    assert bad.size == 0, f"{len(bad)} int32 mismatches, first at {bad[:4].tolist()}"
+    exp = oracle_requant(orc, c, acc, 1)
+    out_h = out.cpu().numpy()
+    bad = np.argwhere(out_h != exp)
+    assert bad.size == 0, f"{len(bad)} u8 mismatches, first at {bad[:4].tolist()}"
+    sat = np.mean((exp == 255) | (exp == c.zp_c))
+    assert sat < 0.8  # outputs are spread, not all clamped
 
 
 @pytest.mark.parametrize("seed", range(32))
