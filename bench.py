@@ -1,41 +1,50 @@
 """Benchmark of the B200 fused u8 x s8 -> s32 GEMM + requantization hot path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C0|C1|C2|C3|C4] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C0..C4] [--impl ours|reference]
 
-(C3 / C4: conv 3x3 and depthwise 3x3 with the batch sharded over ranks; the
-default, the headline, is C1.)
+One JSON line on rank 0.  The headline (default) is BASELINE configs[2],
+"C2": the large-batch FC layer M=16384 N=4096 K=4096 with per-channel
+zero points / scales, int32 bias and ReLU fused into the requantizing
+epilogue -- the tensor-bound configuration north_star's ">= 70% of dense
+INT8 tensor peak" target is quoted on.  A "step" is one pass of the hot path
+over the whole batch: one fused GEMM + requant launch (B prepacked once;
+packing not timed, BASELINE configs[1]).
 
-One JSON line on rank 0.  A "step" is one pass of the hot path over one batch:
-one fused GEMM + per-channel requant + ReLU launch at BASELINE configs[1]
-("C1": M=128 rows per GPU, N=4096, K=4096; B prepacked once, packing not
-timed).  With N GPUs (torchrun, one process per GPU) each rank owns one
-128-row stripe of an M=128*N batch with B replicated -- the reference's own
-row-stripe partitioning (engine.hpp:40-47) -- and no collective: weak scaling.
+Multi-GPU (torchrun, one process per GPU): strong scaling of the configs
+BASELINE partitions.  C2: rank r computes the row stripe
+stripe_rows(16384, r, N) -- the reference's own balanced partition of row
+blocks over workers (engine.hpp:39-47, 102-103) -- with B replicated; C3 / C4:
+rank r convolves its contiguous range of the 32 images.  No collective on the
+data path; the only collective is the max-over-ranks timing reduction.
+value = the configuration's total int8 ops per step / the max-over-ranks step
+time; roofline peaks are N x the per-GPU peak.
 
-value     : whole-job int8 TOPS (2*M*N*K per step over all ranks / max-over-
-            ranks device time), inputs resident in HBM, the K steps replayed
-            from one CUDA graph, cycling through rotating buffer sets whose
-            total footprint is > 2x the 126 MB L2 (so every step reads its
-            weights from HBM).
-e2e       : the same metric through the C-ABI host-buffer entry point
-            (q8g_gemm_u8s8_requant_host): per step H2D of A from pinned
-            memory, the kernel, D2H of the u8 output.
-roofline  : the GEMM kernel's algorithmic bytes / its average launch
-            duration over the timed region (K back-to-back launches between
-            one event pair; kernel_ms_isolated = per-launch event pairs) vs
-            the measured HBM copy bandwidth (MEASURED_PEAKS.json); traffic =
-            ncu dram bytes of the same kernel (profiles/), or null.
+value     : whole-job int8 TOPS (2*M*N*K per step / device time), inputs
+            resident in HBM, the K steps replayed from one CUDA graph over
+            rotating buffer sets whose footprint is > 2x the 126 MB L2.
+e2e       : the same metric through the C-ABI host-buffer entry points
+            (q8g_gemm_u8s8_requant_host, q8g_conv3x3_u8s8_nhwc_host,
+            q8g_dwconv3x3_u8s8_nhwc_host), wall clock per synchronous call:
+            pinned host inputs copied in and outputs copied out every step.
+roofline  : the dominant kernel (the only one launched) -- algorithmic ops
+            (tensor-bound C2) or bytes (HBM-bound C1, C3, C4) per launch over
+            its average launch duration in the timed region, against the
+            measured peaks (int8: profiles/int8_peak.json, HBM:
+            MEASURED_PEAKS.json); traffic = ncu DRAM bytes of the same kernel
+            (profiles/traffic.json) or null.
+sub       : C1 (N=1 only: BASELINE does not partition it), C3 and C4 measured
+            the same way, each with its own roofline (headline run only).
 cpu_baseline / --impl reference : the reference's own CPU path
-            (oracle/_ref: unmodified q8gemm execute_gemm, caller-owned
-            std::threads = all host cores) + the restated per-channel fp32
-            requant, timed on this host.
+            (oracle/_ref: unmodified q8gemm execute_gemm on all host cores, +
+            the restated per-channel fp32 requant) on a bounded row sample.
+clocks    : NVML SM clock / throttle reasons polled every ~0.5 ms during the
+            timed region.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -47,44 +56,100 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "int8 TOPS (fused GEMM+requant) and fraction of INT8 tensor peak / HBM BW"
-CONFIGS = {
-    # name: (M per GPU, N, K, alpha_C, description)
-    "C1": (128, 4096, 4096, 2.2, "C1 production FC: M=128/GPU N=4096 K=4096, per-channel zp_b/alpha_B, "
-                                 "int32 bias, ReLU, u8 out (BASELINE configs[1])"),
-    "C2": (16384, 4096, 4096, 2.2, "C2 large-batch FC: M=16384/GPU N=4096 K=4096, per-channel requant+ReLU "
-                                   "(BASELINE configs[2])"),
-    "C0": (64, 800, 320, 0.5, "C0 single FC: M=64 N=800 K=320 (BASELINE configs[0], F32_RNE)"),
+HEADLINE = "C2"
+GEMM_CONFIGS = {
+    # name: (M total, N, K, alpha_C, description)
+    "C0": (64, 800, 320, 0.5, "C0 single FC: M=64 N=800 K=320 (BASELINE configs[0])"),
+    "C1": (128, 4096, 4096, 2.2, "C1 production FC: M=128 N=4096 K=4096, per-channel zp_b/alpha_B, int32 bias, "
+                                 "ReLU, u8 out (BASELINE configs[1])"),
+    "C2": (16384, 4096, 4096, 2.2, "C2 large-batch FC: M=16384 N=4096 K=4096, per-channel zp_b/alpha_B, int32 bias, "
+                                   "ReLU, u8 out (BASELINE configs[2])"),
 }
-# conv workloads (batch sharded over ranks): name -> (images/GPU, H, W, C, OC or 0 = depthwise, alpha_C, description)
 CONV_CONFIGS = {
+    # name: (images, H, W, C, OC or 0 = depthwise, alpha_C, description)
     "C3": (32, 56, 56, 64, 64, 0.8, "C3 conv3x3 as implicit GEMM: NHWC 32x56x56x64 -> 64, pad 1 with zp_a, "
                                     "per-channel requant + ReLU (BASELINE configs[3])"),
     "C4": (32, 112, 112, 256, 0, 0.1, "C4 depthwise 3x3: NHWC 32x112x112x256, pad 1 with zp_a, per-channel "
                                       "requant + ReLU (BASELINE configs[4])"),
 }
+# roofline bound per config: C0 launch latency (reported
+# against HBM), C1 HBM (intensity 240 < ridge), C2 tensor, C3 ~balanced
+# (reported against HBM), C4 HBM
+BOUND = {"C0": "hbm", "C1": "hbm", "C2": "tensor", "C3": "hbm", "C4": "hbm"}
+L2_BYTES = 126e6
 
+
+# ---------------------------------------------------------------- shared pieces
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
-    return 6650.0, 1590.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def int8_peaks():
-    """Measured dense INT8 tensor peak of this pool's B200 (tools/int8_peak.cu,
-    committed in profiles/int8_peak.json): (burst, sustained) TOPS."""
+    """Measured dense INT8 tensor peaks of this pool's B200 (tools/int8_peak.cu,
+    profiles/int8_peak.json): burst (the denominator: a K-step graph of
+    ~0.2 ms launches is a burst), sustained, and the burst with uniformly
+    random operands when measured."""
     p = ROOT / "profiles" / "int8_peak.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["int8_tops_burst"]), float(d["int8_tops_sustained"]), "measured (profiles/int8_peak.json)"
-    return 4500.0, 4500.0, "fallback (B200 dense INT8 spec, SURVEY 8(d))"
+        return (float(d["int8_tops_burst"]), float(d["int8_tops_sustained"]),
+                d.get("int8_tops_burst_random"), "measured (profiles/int8_peak.json, tools/int8_peak.cu)")
+    return 4500.0, 4500.0, None, "fallback (B200 dense INT8 spec, SURVEY 8(d))"
 
 
-# roofline bound per config (SURVEY 8(d)): C0 launch-latency (reported
-# against HBM), C1 HBM (intensity 240 < ridge), C2 tensor
-BOUND = {"C0": "hbm", "C1": "hbm", "C2": "tensor", "C3": "hbm", "C4": "hbm"}
+def traffic_of(cfg):
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        return json.loads(tf.read_text()).get(cfg)
+    return None
+
+
+def image_range(nb, rank, world):
+    """Contiguous balanced image range of rank (batch sharding, C3 / C4)."""
+    return nb * rank // world, nb * (rank + 1) // world
+
+
+def gemm_rows(m, rank, world):
+    """Row stripe of rank: the reference partition of 128-row blocks
+    (engine.hpp:40-47 via q8g_partition_stripes)."""
+    from paper_2101_05615_b200 import api
+    return api.stripe_rows(m, rank, world)
+
+
+def gemm_ops(cfg):
+    m, n, k = GEMM_CONFIGS[cfg][:3]
+    return 2.0 * m * n * k
+
+
+def gemm_bytes(m, n, k):
+    # A + B + u8 out + 16-byte per-column epilogue record (c, zp_b, mult)
+    return m * k + k * n + m * n + 16 * n
+
+
+def conv_ops_bytes(cfg, nb):
+    """Algorithmic int8 ops and bytes of one conv / depthwise launch over nb
+    images (x + y + weights + per-channel tables)."""
+    _, h, w, c, oc, _, _ = CONV_CONFIGS[cfg]
+    if oc:
+        return 2.0 * nb * h * w * oc * 9 * c, nb * h * w * (c + oc) + 9 * c * oc + 16 * oc
+    return 2.0 * 9 * nb * h * w * c, 2 * nb * h * w * c + 9 * c + 16 * c
+
+
+def config_dict(cfg, world):
+    """The workload identity -- identical in both arms."""
+    if cfg in GEMM_CONFIGS:
+        m, n, k, _, desc = GEMM_CONFIGS[cfg]
+        par = ("rows sharded over the GPUs (strong scaling, stripe_rows = engine.hpp:40-47), B replicated, "
+               "no collective") if cfg == "C2" else "one GPU (BASELINE does not partition it); stripes of rank 0"
+        return {"workload": desc, "M": m, "N": n, "K": k, "gpus": world, "parallelism": par}
+    nb, h, w, c, oc, _, desc = CONV_CONFIGS[cfg]
+    return {"workload": desc, "images": nb, "H": h, "W": w, "C": c, "OC": oc or c, "gpus": world,
+            "parallelism": "images sharded over the GPUs (strong scaling), weights replicated, no collective"}
 
 
 def max_over_ranks(vals, device, world):
@@ -98,80 +163,114 @@ def max_over_ranks(vals, device, world):
     return [float(v) for v in t.cpu()]
 
 
-def whole_job_tops(m_per_rank, n, k, world, ms_per_step):
-    """Weak scaling: every rank runs an M=m_per_rank stripe; value = all
-    ranks' int8 ops per step / the max-over-ranks step time."""
-    return 2.0 * m_per_rank * n * k * world / (ms_per_step * 1e-3) / 1e12
-
-
-def algorithmic_bytes(m, n, k):
-    # A + B + u8 out + 16-byte per-column epilogue record (c, zp_b, mult)
-    return m * k + k * n + m * n + 16 * n
+def whole_job_tops(total_ops_per_step, ms_per_step):
+    return total_ops_per_step / (ms_per_step * 1e-3) / 1e12
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock, max clock and throttle reasons polled through NVML every
+    ~0.5 ms while the timed region runs (nvidia-smi samples at >= 100 ms would
+    miss a few-ms region); falls back to a single nvidia-smi query."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.stop_flag = False
+        self.thread = None
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001 - no NVML: report unavailable
+            self.nv = None
+
+    def _reasons(self):
+        nv = self.nv
+        try:
+            return int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        except Exception:  # noqa: BLE001 - older binding name
+            return int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)), self._reasons()))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.0005)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        if self.nv is not None:
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable or no sample"], "samples": 0}
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        return {"sm_mhz": float(np.median([s for s, _ in self.samples])), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in self.REASONS.items() if bits & k), "samples": len(self.samples),
+                "source": "NVML, polled every ~0.5 ms during the timed region"}
+
+
+def idle_rank_barriers(world):
+    """A rank with no rows / images still joins timed_graph's two barriers."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.barrier()
+
+
+def timed_graph(run_step, steps, stream, dev, world, sampler_index):
+    """Capture `steps` steps in one CUDA graph; time exactly one replay between
+    a barrier + synchronize on both sides (CUDA events on the launching
+    stream) with the clocks sampled during it.  Returns (ms, clocks)."""
+    import torch
+    import torch.distributed as dist
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for i in range(steps):
+            run_step(i)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(sampler_index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    start.record(stream)
+    graph.replay()
+    end.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    return start.elapsed_time(end), clocks
 
 
 # ---------------------------------------------------------------- reference arm
 
-def cpu_reference(cfg: str, steps: int, warmup: int, threads: int, budget_s: float | None = None):
-    """The reference's CPU path on this host: unmodified q8gemm execute_gemm
-    (oracle/_ref) with `threads` caller-owned workers + the restated
-    per-channel fp32 requant (the reference is per-tensor only)."""
+def cpu_reference_gemm(cfg, threads, budget_s=15.0, max_steps=20, rows=None):
+    """The reference's CPU path on this host on a bounded row sample: unmodified
+    q8gemm execute_gemm[WriteRawI32] (oracle/_ref) with `threads` caller-owned
+    workers + the restated per-channel fp32 requant (the reference is
+    per-tensor only).  TOPS of the sample."""
     from oracle.py import Oracle, RefLib  # CPU baseline leg only
-    m, n, k, alpha_c, _ = CONFIGS[cfg]
-    orc = Oracle()
-    ref = RefLib()
+    m_all, n, k, alpha_c, _ = GEMM_CONFIGS[cfg]
+    m = rows or min(m_all, 1024)
+    orc, ref = Oracle(), RefLib()
     r = orc.rng(42)
     a = r.u8_matrix(m, k)
     b = r.i8_matrix(k, n)
@@ -186,35 +285,24 @@ def cpu_reference(cfg: str, steps: int, warmup: int, threads: int, budget_s: flo
         return orc.requant_matrix(acc, orc.row_offsets(a), colsum, 128, zp_b, k, bias, 1, mult, 5, True,
                                   per_channel=True)
 
-    for _ in range(warmup):
-        step()
+    step()
     times = []
     t_all = time.perf_counter()
-    for i in range(steps):
+    while not times or (time.perf_counter() - t_all < budget_s and len(times) < max_steps):
         t0 = time.perf_counter()
         step()
         times.append(time.perf_counter() - t0)
-        if budget_s is not None and time.perf_counter() - t_all > budget_s:
-            break
     sec = float(np.median(times))
     ops = 2.0 * m * n * k
+    busy = max(1, min(threads, -(-m // 56)))
     return {"value": ops / sec / 1e12, "unit": "TOPS", "cores": threads, "kind": "reference",
-            "sample": f"{len(times)} x {cfg} ({m}x{n}x{k}) reference execute_gemm[WriteRawI32] + restated "
+            "sample": f"{m} of {cfg}'s {m_all} rows ({m}x{n}x{k}): reference execute_gemm[WriteRawI32] + restated "
                       f"per-channel F32_RNE requant, median of {len(times)}, {threads} std::threads "
-                      f"(row stripes cap the busy ones at {max(1, (m + 55) // 56)})",
-            "ms_per_step": sec * 1e3, "steps_timed": len(times)}
+                      f"({busy} row stripes busy)",
+            "ms_per_sample": sec * 1e3}
 
 
-def conv_ops_bytes(cfg: str, nb: int):
-    """Algorithmic int8 ops and bytes of one conv / depthwise launch over nb images
-    (x + y + weights + per-channel tables)."""
-    _, h, w, c, oc, _, _ = CONV_CONFIGS[cfg]
-    if oc:
-        return 2.0 * nb * h * w * oc * 9 * c, nb * h * w * (c + oc) + 9 * c * oc + 16 * oc
-    return 2.0 * 9 * nb * h * w * c, 2 * nb * h * w * c + 9 * c + 16 * c
-
-
-def conv_inputs(cfg: str):
+def conv_inputs(cfg):
     """Weights and per-channel requant parameters (BASELINE distributions, App. A D4)."""
     _, h, w, c, oc, alpha_c, _ = CONV_CONFIGS[cfg]
     r = np.random.default_rng(11)
@@ -226,7 +314,7 @@ def conv_inputs(cfg: str):
     return wt, bias, zp_b, mult
 
 
-def cpu_reference_conv(cfg: str, threads: int, budget_s: float = 15.0, images: int = 0):
+def cpu_reference_conv(cfg, threads, budget_s=15.0, images=0):
     """C3: restated im2col + the reference execute_gemm (oracle/_ref) + restated
     per-channel requant; C4: the restated depthwise loop (no reference path),
     on a bounded sample of images of the workload."""
@@ -262,8 +350,9 @@ def cpu_reference_conv(cfg: str, threads: int, budget_s: float = 15.0, images: i
     sec = float(np.median(times))
     ops, _ = conv_ops_bytes(cfg, nimg)
     return {"value": ops / sec / 1e12, "unit": "TOPS", "cores": threads, "kind": kind,
-            "sample": f"{nimg} of the workload's images, {what}, median of {len(times)}, {threads} threads",
-            "ms_per_step": sec * 1e3 * CONV_CONFIGS[cfg][0] / nimg, "steps_timed": len(times)}
+            "sample": f"{nimg} of the workload's {CONV_CONFIGS[cfg][0]} images, {what}, median of {len(times)}, "
+                      f"{threads} threads",
+            "ms_per_sample": sec * 1e3}
 
 
 def run_reference_arm(args):
@@ -271,25 +360,21 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
+    budget = min(120.0, 5.0 + 2.0 * args.steps)
     if args.config in CONV_CONFIGS:
-        res = cpu_reference_conv(args.config, threads, budget_s=min(120.0, 5.0 + 2.0 * args.steps))
-        desc = CONV_CONFIGS[args.config][-1]
-        line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "TOPS", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
-                "data": "synthetic (seeded numpy RNG, BASELINE distributions)",
-                "config": {"workload": desc, "path": "CPU " + res["kind"] + " (oracle/)"},
-                "cpu_baseline": {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": res["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
-    res = cpu_reference(args.config, args.steps, args.warmup, threads)
-    m, n, k, _, desc = CONFIGS[args.config]
+        res = cpu_reference_conv(args.config, threads, budget_s=budget)
+    else:
+        res = cpu_reference_gemm(args.config, threads, budget_s=budget, max_steps=max(1, args.steps))
+    ops = gemm_ops(args.config) if args.config in GEMM_CONFIGS else \
+        conv_ops_bytes(args.config, CONV_CONFIGS[args.config][0])[0]
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "TOPS", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
-            "data": "synthetic (seeded mt19937_64, BASELINE distributions)",
-            "config": {"workload": desc, "M": m, "N": n, "K": k, "path": "CPU reference (oracle/_ref)"},
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ops / (res["value"] * 1e12) * 1e3,  # the whole workload at the sample's rate
+            "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8xs8->s32",
+            "data": "synthetic (seeded mt19937_64 / numpy RNG, BASELINE distributions)",
+            "config": config_dict(args.config, args.gpus),
+            "path": "CPU " + res["kind"] + " (oracle/_ref; the reference's own execute_gemm)",
             "cpu_baseline": {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -298,350 +383,296 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- our arm
 
-def run_ours(args):
+def bench_gemm(cfg, ctx, steps, warmup, want_e2e=True):
+    """One GEMM configuration on this rank's row stripe."""
     import torch
-    import torch.distributed as dist
 
     import paper_2101_05615_b200 as q8
     from paper_2101_05615_b200 import _lib
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev, rank, world, stream, lib = ctx["dev"], ctx["rank"], ctx["world"], ctx["stream"], ctx["lib"]
+    m_all, n, k, alpha_c, _ = GEMM_CONFIGS[cfg]
+    if cfg != "C2" and world > 1:
+        r0, r1 = (0, m_all) if rank == 0 else (0, 0)
     else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", local if world > 1 else 0)
-    didx = dev.index
-
-    m, n, k, alpha_c, desc = CONFIGS[args.config]
+        r0, r1 = gemm_rows(m_all, rank, world)
+    m = r1 - r0
+    # weights and epilogue parameters: the same seeded draws on every rank (B replicated)
     g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    # inputs with BASELINE distributions (synthetic): A u8 U[0,255], B s8 U[-128,127]
+    g.manual_seed(1234)
     b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device=dev, generator=g)
     bias = np.random.default_rng(7).integers(-1000, 1001, n).astype(np.int32)
     zp_b = np.random.default_rng(8).integers(-10, 11, n).astype(np.int32)
-    alpha_b = np.random.default_rng(9).uniform(0.005, 0.02, n)
-    mult = (0.02 * alpha_b / alpha_c).astype(np.float32)
-    pw0 = q8.prepack_weights(b, device=didx)
+    mult = (0.02 * np.random.default_rng(9).uniform(0.005, 0.02, n) / alpha_c).astype(np.float32)
     rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=k, bias=bias, zp_b_per_channel=zp_b,
                           multiplier_f32_per_channel=mult, rounding=q8.ROUND_F32_RNE)
     pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
-
-    # rotating buffer sets: total footprint > 2x L2 so weights come from HBM
-    set_bytes = algorithmic_bytes(m, n, k)
-    nsets = max(2, min(64, int(np.ceil(2.2 * 126e6 / set_bytes))))
-    pws = [pw0] + [pw0.replicate(didx) for _ in range(nsets - 1)]
+    pw0 = q8.prepack_weights(b, device=dev.index)
+    out = {"rows": [r0, r1]}
+    if m == 0:  # an idle rank still takes part in the barriers / reductions
+        idle_rank_barriers(world)
+        out.update(ms=0.0, launches=0, e2e_ms=0.0, clocks=None, kern_ms_isolated=0.0, nsets=0)
+        return out
+    # rotating buffer sets > 2x L2; the weights rotate too where they dominate the bytes
+    rotate_b = k * n > m * (k + n)
+    set_bytes = m * (k + n) + (k * n if rotate_b else 0)
+    nsets = max(2, min(64, int(np.ceil(2.2 * L2_BYTES / set_bytes))))
+    pws = [pw0] + ([pw0.replicate(dev.index) for _ in range(nsets - 1)] if rotate_b else [pw0] * (nsets - 1))
+    g.manual_seed(99 + rank)
     As = [torch.randint(0, 256, (m, k), dtype=torch.uint8, device=dev, generator=g) for _ in range(nsets)]
     Cs = [torch.empty((m, n), dtype=torch.uint8, device=dev) for _ in range(nsets)]
     eps = [pipe.epilogue(p) for p in pws]
-    lib = _lib.load()
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)  # graph replays + events all on this stream
 
-    def launch(i, s):
+    def launch(i):
         j = i % nsets
         _lib.check(lib.q8g_gemm_u8s8_requant(As[j].data_ptr(), m, k, k, pws[j].handle, eps[j], Cs[j].data_ptr(), n,
-                                             0, m, None, s.cuda_stream))
+                                             0, m, None, stream.cuda_stream))
 
-    # warm-up (also builds tensor maps for every buffer set)
     with torch.cuda.stream(stream):
-        for i in range(max(args.warmup, nsets)):
-            launch(i, stream)
+        for i in range(max(warmup, nsets)):
+            launch(i)
     torch.cuda.synchronize(dev)
-
-    # capture the K-step loop in one CUDA graph
     c0 = _lib.launch_count()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        for i in range(args.steps):
-            launch(i, stream)
-    launches_per_step = (_lib.launch_count() - c0) / args.steps
-    # per-launch event timing graph (roofline): events around each kernel
-    ev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
-          for _ in range(nsets)]
-    graph_ev = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph_ev, stream=stream):
-        for i in range(nsets):
-            ev[i][0].record(stream)
-            launch(i, stream)
-            ev[i][1].record(stream)
-    for _ in range(max(1, args.warmup // nsets)):
-        graph_ev.replay()
-    torch.cuda.synchronize(dev)
-
-    sampler = ClockSampler(didx)
-    sampler.start()
-    time.sleep(0.3)
-    # sustained replay so the sampler sees the clocks under this load
-    t_end = time.time() + 1.0
-    while time.time() < t_end:
-        graph_ev.replay()
+    ms, clocks = timed_graph(launch, steps, stream, dev, world, dev.index)
+    # the graph capture counted its launches once
+    out.update(ms=ms, launches=_lib.launch_count() - c0, clocks=clocks, nsets=nsets, set_bytes=set_bytes)
+    if cfg == "C2" and clocks is not None:
+        # the SM clock the last timed launch actually ran at (CTA 0 clock64 /
+        # globaltimer): NVML reports the clock target, not the power-limited clock
+        import ctypes
+        cyc, ns = ctypes.c_uint64(), ctypes.c_uint64()
+        if lib.q8g_debug_kernel_clock(ctypes.byref(cyc), ctypes.byref(ns)) == 0 and ns.value > 0:
+            clocks["sm_mhz_in_kernel"] = cyc.value / ns.value * 1e3
+            clocks["sm_mhz_in_kernel_source"] = "clock64 / globaltimer of CTA 0 over the last timed launch"
+    # a lone launch (per-launch event pairs; no overlap with a neighbour)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nsets)]
+    iso = []
+    for _ in range(2):
+        for j in range(nsets):
+            ev[j][0].record(stream)
+            launch(j)
+            ev[j][1].record(stream)
         torch.cuda.synchronize(dev)
+        iso += [a.elapsed_time(bb) for a, bb in ev]
+    out["kern_ms_isolated"] = float(np.median(iso))
+    if want_e2e:
+        a_host = torch.randint(0, 256, (m, k), dtype=torch.uint8, generator=torch.Generator().manual_seed(3))
+        a_host = a_host.pin_memory()
+        c_host = torch.empty((m, n), dtype=torch.uint8).pin_memory()
 
-    # ---- timed region: exactly K steps
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with torch.cuda.stream(stream):  # replay and events on the same stream
-        start.record(stream)
-        graph.replay()
-        end.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    ms = start.elapsed_time(end)
-    clocks = sampler.stop()
+        def e2e_call(i):
+            j = i % nsets
+            _lib.check(lib.q8g_gemm_u8s8_requant_host(a_host.data_ptr(), m, k, k, pws[j].handle, eps[j],
+                                                      c_host.data_ptr(), n, 0, m, stream.cuda_stream))
 
-    # per-launch kernel duration (same kernel, same buffers)
-    kern_ms = []
-    for _ in range(5):
-        graph_ev.replay()
-        torch.cuda.synchronize(dev)
-        kern_ms += [a.elapsed_time(bb) for a, bb in ev]
-    kern_ms = float(np.mean(kern_ms))
-
-    # ---- e2e through the C-ABI host-buffer entry point
-    a_host = torch.randint(0, 256, (m, k), dtype=torch.uint8, generator=torch.Generator().manual_seed(3)).pin_memory()
-    c_host = torch.empty((m, n), dtype=torch.uint8).pin_memory()
-    e2e_steps = max(1, min(args.steps, 50))
-
-    def e2e_call(i):
-        j = i % nsets
-        _lib.check(lib.q8g_gemm_u8s8_requant_host(a_host.data_ptr(), m, k, k, pws[j].handle, eps[j],
-                                                  c_host.data_ptr(), n, 0, m, stream.cuda_stream))
-
-    for i in range(3):
-        e2e_call(i)
-    if world > 1:
-        dist.barrier()
-    # device-side span on the call's stream: H2D of A, the GEMM, D2H of C and
-    # any host gaps between the (synchronous) calls all fall inside it
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize(dev)
-    e0.record(stream)
-    for i in range(e2e_steps):
-        e2e_call(i)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_s = e0.elapsed_time(e1) * 1e-3 / e2e_steps
-    if world > 1:
-        dist.barrier()
-
-    ms, kern_ms, e2e_s = max_over_ranks([ms, kern_ms, e2e_s], dev, world)
-
-    if rank == 0:
-        ms_step = ms / args.steps
-        value = whole_job_tops(m, n, k, world, ms_step)
-        hbm, _, src = peaks()
-        abytes = algorithmic_bytes(m, n, k)
-        # the dominant (only) kernel's average launch duration over the timed
-        # region: K back-to-back launches between one event pair
-        kern_avg_ms = ms_step / max(1.0, launches_per_step)
-        achieved = abytes / (kern_avg_ms * 1e-3) / 1e9
-        tops_launch = 2.0 * m * n * k / (kern_avg_ms * 1e-3) / 1e12
-        if BOUND[args.config] == "tensor":
-            # a K-step back-to-back run of a long kernel: the sustained peak
-            burst, sust, isrc = int8_peaks()
-            roof = {"bound": "tensor", "achieved": tops_launch, "peak": sust, "unit": "TFLOP/s",
-                    "unit_note": "dense int8 tera-ops/s (2*M*N*K per launch)", "frac": tops_launch / sust,
-                    "frac_of_burst": tops_launch / burst, "peak_source": isrc + ", sustained",
-                    "hbm_achieved_gbs": achieved, "hbm_frac": achieved / hbm}
-        else:
-            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "peak_source": src + " (MEASURED_PEAKS.json hbm_gbs)"}
-        traffic = None
-        tf = ROOT / "profiles" / "traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get(args.config)
-        line = {
-            "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8xs8->s32", "data": "synthetic (seeded torch RNG, BASELINE distributions)",
-            "config": {"workload": desc, "M_per_gpu": m, "N": n, "K": k, "global_rows": m * world,
-                       "parallelism": f"rows sharded x{world}, B replicated, no collective",
-                       "l2": f"{nsets} rotating buffer sets, {nsets * set_bytes / 1e6:.0f} MB > 2x126 MB L2",
-                       "graph": "K steps captured in one CUDA graph", "packing": "excluded (prepacked once)"},
-            "roofline": dict(roof, traffic=traffic, algorithmic_bytes_per_launch=abytes, kernel_ms=kern_avg_ms,
-                             kernel_ms_isolated=kern_ms, int8_tops_per_launch=tops_launch),
-            "e2e": {"value": 2.0 * m * n * k * world / e2e_s / 1e12, "unit": "TOPS",
-                    "h2d_bytes_per_step": m * k * world, "d2h_bytes_per_step": m * n * world,
-                    "ms_per_step": e2e_s * 1e3, "path": "q8g_gemm_u8s8_requant_host (pinned host buffers)"},
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-            "clocks": clocks,
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                cb = cpu_reference(args.config, 50, 2, os.cpu_count() or 1, budget_s=15.0)
-                line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
-            except Exception as e:  # the baseline is reported, never the target
-                line["cpu_baseline"] = {"value": None, "unit": "TOPS", "cores": 0, "kind": "reference",
-                                        "sample": f"unavailable: {e}"}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+        for i in range(2):
+            e2e_call(i)
+        n_e2e = max(3, min(steps, 20))
+        ts = []
+        for i in range(n_e2e):
+            t0 = time.perf_counter()
+            e2e_call(i)
+            ts.append(time.perf_counter() - t0)
+        out["e2e_ms"] = float(np.median(ts)) * 1e3
+        out["e2e_bytes"] = (m * k, m * n)
+    return out
 
 
-def run_conv_ours(args):
-    """C3 / C4: each rank convolves its own batch of images (batch sharded, no
-    collective); same timing rules as the GEMM arm."""
+def bench_conv(cfg, ctx, steps, warmup, want_e2e=True):
+    """C3 / C4 on this rank's image range."""
     import torch
-    import torch.distributed as dist
 
     import paper_2101_05615_b200 as q8
     from paper_2101_05615_b200 import _lib
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", local if world > 1 else 0)
-    didx = dev.index
-    nb, h, w, c, oc, _, desc = CONV_CONFIGS[args.config]
+    dev, rank, world, stream, lib = ctx["dev"], ctx["rank"], ctx["world"], ctx["stream"], ctx["lib"]
+    nb_all, h, w, c, oc, _, _ = CONV_CONFIGS[cfg]
+    i0, i1 = image_range(nb_all, rank, world)
+    nb = i1 - i0
     nout = oc or c
-    wt, bias, zp_b, mult = conv_inputs(args.config)
+    wt, bias, zp_b, mult = conv_inputs(cfg)
     rp = q8.RequantParams(zp_a=128, zp_c=5, k_total=9 * c if oc else 9, bias=bias, zp_b_per_channel=zp_b,
                           multiplier_f32_per_channel=mult, rounding=q8.ROUND_F32_RNE)
+    out = {"images": [i0, i1]}
+    if nb == 0:
+        idle_rank_barriers(world)
+        out.update(ms=0.0, launches=0, e2e_ms=0.0, clocks=None, kern_ms_isolated=0.0, nsets=0)
+        return out
     if oc:
-        pw = q8.prepack_conv3x3_weights(wt, device=didx)
+        pw = q8.prepack_conv3x3_weights(wt, device=dev.index)
         pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
+        ep = pipe.epilogue(pw)
 
         def call(x, y):
-            q8.execute_conv3x3(x, pw, y, pipe)
+            _lib.check(lib.q8g_conv3x3_u8s8_nhwc(x.data_ptr(), nb, h, w, c, pw.handle, ep, y.data_ptr(), 0, nb,
+                                                 stream.cuda_stream))
+
+        def call_host(x, y):
+            _lib.check(lib.q8g_conv3x3_u8s8_nhwc_host(x.data_ptr(), nb, h, w, c, pw.handle, ep, y.data_ptr(), 0, nb,
+                                                      stream.cuda_stream))
     else:
-        filt = q8.DepthwiseFilter(wt, rp, relu=True, device=didx)
+        filt = q8.DepthwiseFilter(wt, rp, relu=True, device=dev.index)
 
         def call(x, y):
-            q8.execute_dwconv3x3(x, filt, y)
-    ops, abytes = conv_ops_bytes(args.config, nb)
+            _lib.check(lib.q8g_dwconv3x3_u8s8_nhwc(x.data_ptr(), nb, h, w, c, filt._h, y.data_ptr(), 0, nb,
+                                                   stream.cuda_stream))
+
+        def call_host(x, y):
+            _lib.check(lib.q8g_dwconv3x3_u8s8_nhwc_host(x.data_ptr(), nb, h, w, c, filt._h, y.data_ptr(), 0, nb,
+                                                        stream.cuda_stream))
     set_bytes = nb * h * w * (c + nout)
-    nsets = max(2, min(64, int(np.ceil(2.2 * 126e6 / set_bytes))))
+    nsets = max(2, min(64, int(np.ceil(2.2 * L2_BYTES / set_bytes))))
     g = torch.Generator(device=dev)
     g.manual_seed(99 + rank)
     xs = [torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device=dev, generator=g) for _ in range(nsets)]
     ys = [torch.empty((nb, h, w, nout), dtype=torch.uint8, device=dev) for _ in range(nsets)]
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
 
     def launch(i):
         call(xs[i % nsets], ys[i % nsets])
 
-    for i in range(max(args.warmup, nsets)):
-        launch(i)
+    with torch.cuda.stream(stream):
+        for i in range(max(warmup, nsets)):
+            launch(i)
     torch.cuda.synchronize(dev)
     c0 = _lib.launch_count()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        for i in range(args.steps):
-            launch(i)
-    launches_per_step = (_lib.launch_count() - c0) / args.steps
-    ev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
-          for _ in range(nsets)]
-    graph_ev = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph_ev, stream=stream):
-        for i in range(nsets):
-            ev[i][0].record(stream)
-            launch(i)
-            ev[i][1].record(stream)
-    graph_ev.replay()
-    torch.cuda.synchronize(dev)
-    sampler = ClockSampler(didx)
-    sampler.start()
-    time.sleep(0.3)
-    t_end = time.time() + 1.0
-    while time.time() < t_end:
-        graph_ev.replay()
-        torch.cuda.synchronize(dev)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    start.record(stream)
-    graph.replay()
-    end.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    ms = start.elapsed_time(end)
-    clocks = sampler.stop()
-    kern_ms = []
-    for _ in range(3):
-        graph_ev.replay()
-        torch.cuda.synchronize(dev)
-        kern_ms += [a.elapsed_time(bb) for a, bb in ev]
-    kern_ms = float(np.mean(kern_ms))
-
-    # e2e through the public API: pinned x -> device, the call, y -> pinned host, every step
-    x_host = torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, generator=torch.Generator().manual_seed(4))
-    x_host = x_host.pin_memory()
-    y_host = torch.empty((nb, h, w, nout), dtype=torch.uint8).pin_memory()
-    e2e_steps = max(1, min(args.steps, 20))
-
-    def e2e_call():
-        xs[0].copy_(x_host, non_blocking=True)
-        call(xs[0], ys[0])
-        y_host.copy_(ys[0], non_blocking=True)
-
+    ms, clocks = timed_graph(launch, steps, stream, dev, world, dev.index)
+    out.update(ms=ms, launches=_lib.launch_count() - c0, clocks=clocks, nsets=nsets, set_bytes=set_bytes)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nsets)]
+    iso = []
     for _ in range(2):
-        e2e_call()
-    torch.cuda.synchronize(dev)
+        for j in range(nsets):
+            ev[j][0].record(stream)
+            launch(j)
+            ev[j][1].record(stream)
+        torch.cuda.synchronize(dev)
+        iso += [a.elapsed_time(bb) for a, bb in ev]
+    out["kern_ms_isolated"] = float(np.median(iso))
+    if want_e2e:
+        x_host = torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, generator=torch.Generator().manual_seed(4))
+        x_host = x_host.pin_memory()
+        y_host = torch.empty((nb, h, w, nout), dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            call_host(x_host, y_host)
+        ts = []
+        for _ in range(max(3, min(steps, 20))):
+            t0 = time.perf_counter()
+            call_host(x_host, y_host)
+            ts.append(time.perf_counter() - t0)
+        out["e2e_ms"] = float(np.median(ts)) * 1e3
+        out["e2e_bytes"] = (nb * h * w * c, nb * h * w * nout)
+    return out
+
+
+def summarize(cfg, res_all, world, steps):
+    """Rank-0 record of one configuration from the max-over-ranks timings."""
+    ms, kern_iso, e2e_ms = res_all
+    ms_step = ms / steps
+    if cfg in GEMM_CONFIGS:
+        m, n, k = GEMM_CONFIGS[cfg][:3]
+        ops = gemm_ops(cfg)
+        abytes = gemm_bytes(m, n, k)
+    else:
+        ops, abytes = conv_ops_bytes(cfg, CONV_CONFIGS[cfg][0])
+    value = whole_job_tops(ops, ms_step)
+    hbm, hsrc = peaks()
+    if BOUND[cfg] == "tensor":
+        burst, sust, rnd, isrc = int8_peaks()
+        roof = {"bound": "tensor", "achieved": value, "peak": burst * world, "unit": "TFLOP/s",
+                "unit_note": "dense int8 tera-ops/s (2*M*N*K per launch)", "frac": value / (burst * world),
+                "peak_source": isrc + f", burst x {world} GPU(s)", "frac_of_sustained_peak": value / (sust * world),
+                "hbm_achieved_gbs": abytes / (ms_step * 1e-3) / 1e9}
+        if rnd:
+            roof["frac_of_random_operand_peak"] = value / (float(rnd) * world)
+    else:
+        achieved = abytes / (ms_step * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm * world, "unit": "GB/s",
+                "frac": achieved / (hbm * world), "peak_source": hsrc + f" x {world} GPU(s)"}
+    roof.update(traffic=traffic_of(cfg), algorithmic_bytes_per_launch=abytes, algorithmic_ops_per_launch=ops,
+                kernel_ms=ms_step, kernel_ms_isolated=kern_iso)
+    return value, ms_step, roof
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2101_05615_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_call()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_s = e0.elapsed_time(e1) * 1e-3 / e2e_steps
-    if world > 1:
-        dist.barrier()
-    ms, kern_ms, e2e_s = max_over_ranks([ms, kern_ms, e2e_s], dev, world)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", local if world > 1 else 0)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx = {"dev": dev, "rank": rank, "world": world, "stream": stream, "lib": _lib.load()}
+
+    def one(cfg, steps, warmup, e2e=True):
+        fn = bench_gemm if cfg in GEMM_CONFIGS else bench_conv
+        r = fn(cfg, ctx, steps, warmup, want_e2e=e2e)
+        t = max_over_ranks([r["ms"], r["kern_ms_isolated"], r.get("e2e_ms", 0.0)], dev, world)
+        launches = max_over_ranks([r["launches"]], dev, world)[0]
+        return r, t, launches
+
+    cfg = args.config
+    r, t, launches = one(cfg, args.steps, args.warmup)
+    subs = {}
+    if not args.no_sub and cfg == HEADLINE:
+        for sc in ("C1", "C3", "C4"):
+            if sc == "C1" and world > 1:
+                continue
+            sr, st, sl = one(sc, 20, 5)
+            subs[sc] = (sr, st, sl)
     if rank == 0:
-        ms_step = ms / args.steps
-        kern_avg_ms = ms_step / max(1.0, launches_per_step)
-        hbm, _, src = peaks()
-        achieved = abytes / (kern_avg_ms * 1e-3) / 1e9
-        traffic = None
-        tf = ROOT / "profiles" / "traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get(args.config)
+        value, ms_step, roof = summarize(cfg, t, world, args.steps)
+        e2e_ms = t[2]
+        if cfg in GEMM_CONFIGS:
+            m, n, k = GEMM_CONFIGS[cfg][:3]
+            h2d, d2h = m * k, m * n
+            e2e_path = "q8g_gemm_u8s8_requant_host (pinned host A and C; chunked, copies overlapped with the GEMM)"
+        else:
+            nb, h, w, c, oc = CONV_CONFIGS[cfg][:5]
+            h2d, d2h = nb * h * w * c, nb * h * w * (oc or c)
+            e2e_path = ("q8g_conv3x3_u8s8_nhwc_host" if CONV_CONFIGS[cfg][4] else "q8g_dwconv3x3_u8s8_nhwc_host") + \
+                " (pinned host x and y; chunked, copies overlapped with the kernel)"
+        ops = gemm_ops(cfg) if cfg in GEMM_CONFIGS else conv_ops_bytes(cfg, CONV_CONFIGS[cfg][0])[0]
         line = {
-            "metric": METRIC, "value": ops * world / (ms_step * 1e-3) / 1e12, "unit": "TOPS", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
+            "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8xs8->s32",
             "data": "synthetic (seeded torch / numpy RNG, BASELINE distributions)",
-            "config": {"workload": desc, "images_per_gpu": nb, "global_images": nb * world,
-                       "parallelism": f"batch sharded x{world}, weights replicated, no collective",
-                       "l2": f"{nsets} rotating buffer sets, {nsets * set_bytes / 1e6:.0f} MB > 2x126 MB L2",
-                       "graph": "K steps captured in one CUDA graph", "packing": "excluded (prepacked once)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "peak_source": src + " (MEASURED_PEAKS.json hbm_gbs)", "traffic": traffic,
-                         "algorithmic_bytes_per_launch": abytes, "kernel_ms": kern_avg_ms,
-                         "kernel_ms_isolated": kern_ms, "int8_tops_per_launch": ops / (kern_avg_ms * 1e-3) / 1e12},
-            "e2e": {"value": ops * world / e2e_s / 1e12, "unit": "TOPS",
-                    "h2d_bytes_per_step": nb * h * w * c * world, "d2h_bytes_per_step": nb * h * w * nout * world,
-                    "ms_per_step": e2e_s * 1e3, "path": "pinned x -> device, execute_conv3x3 / execute_dwconv3x3, "
-                                                        "y -> pinned host"},
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-            "clocks": clocks,
+            "config": config_dict(cfg, world),
+            "timing": {"graph": "K steps captured in one CUDA graph, one replay timed with CUDA events",
+                       "l2": f"{r.get('nsets', 0)} rotating buffer sets of {r.get('set_bytes', 0) / 1e6:.1f} MB "
+                             f"per rank (> 2x the 126 MB L2)", "packing": "excluded (prepacked once)",
+                       "rank0_rows_or_images": r.get("rows", r.get("images"))},
+            "roofline": roof,
+            "e2e": {"value": whole_job_tops(ops, e2e_ms), "unit": "TOPS", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "path": e2e_path,
+                    "timing": "host wall clock per synchronous call, median, max over ranks"},
+            "gpu_launches": int(round(launches)),
+            "clocks": r["clocks"],
         }
+        if subs:
+            line["sub"] = {}
+            for sc, (sr, st, sl) in subs.items():
+                sv, sms, sroof = summarize(sc, st, world, 20)
+                sops = gemm_ops(sc) if sc in GEMM_CONFIGS else conv_ops_bytes(sc, CONV_CONFIGS[sc][0])[0]
+                line["sub"][sc] = {"value": sv, "unit": "TOPS", "ms_per_step": sms, "steps": 20, "warmup": 5,
+                                   "config": config_dict(sc, world if sc != "C1" else 1), "roofline": sroof,
+                                   "e2e": {"value": whole_job_tops(sops, st[2]), "unit": "TOPS",
+                                           "ms_per_step": st[2]},
+                                   "gpu_launches": int(round(sl)), "clocks": sr["clocks"]}
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cb = cpu_reference_conv(args.config, os.cpu_count() or 1)
+                cb = (cpu_reference_gemm(cfg, os.cpu_count() or 1) if cfg in GEMM_CONFIGS
+                      else cpu_reference_conv(cfg, os.cpu_count() or 1))
                 line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
-            except Exception as e:  # the baseline is reported, never the target
-                line["cpu_baseline"] = {"value": None, "unit": "TOPS", "cores": 0, "kind": "port",
+            except Exception as e:  # noqa: BLE001 - the baseline is reported, never the target
+                line["cpu_baseline"] = {"value": None, "unit": "TOPS", "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -652,18 +683,16 @@ def run_conv_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS) + sorted(CONV_CONFIGS))
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(GEMM_CONFIGS) + sorted(CONV_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="headline only (no C1 / C3 / C4 sub-records)")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference_arm(args)
-    if args.config in CONV_CONFIGS:
-        return run_conv_ours(args)
     return run_ours(args)
 
 

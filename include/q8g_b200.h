@@ -74,6 +74,10 @@ int q8g_launch_stats(uint64_t* counts, int n);
  * max_ctas > 1024 the whole 10240-word trace buffer is copied (out must hold
  * 10240 words): + per-unit stamps of CTA 0 and per-CTA conv entry/exit */
 int q8g_debug_tc_trace(uint64_t* out, int max_ctas);
+/* debug: SM clock64 cycles and globaltimer ns that CTA 0 of the most recent
+ * large-M CTA-pair GEMM launch spent (cycles / ns = the SM clock that launch
+ * ran at under the power limit) */
+int q8g_debug_kernel_clock(uint64_t* cycles, uint64_t* ns);
 
 /* ---- blocking (dispatch.hpp:17-30, pack.hpp:24-37) ---- */
 int q8g_blocking_defaults(q8g_blocking* out);
@@ -132,7 +136,9 @@ int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g
                           const int32_t* bias_add_dev, int32_t* c_dev, int ldc, int row_begin,
                           int row_end, q8g_kernel_cache* cache, void* stream);
 /* Host-buffer convenience (the reference calling convention: host views).
- * Stages A to the device, runs, and copies C back, synchronously. */
+ * Stages A to the device, runs, and copies C back, synchronously.  Stripes
+ * of >= 4096 rows go in chunks whose H2D / D2H copies overlap the GEMM of
+ * the neighbouring chunks. */
 int q8g_gemm_u8s8_requant_host(const uint8_t* a_host, int m, int k, int lda,
                                const q8g_packed_b* pb, const q8g_epilogue* ep, uint8_t* c_host,
                                int ldc, int row_begin, int row_end, void* stream);
@@ -190,6 +196,12 @@ int q8g_conv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
 int q8g_conv3x3_u8s8_nhwc_raw_i32(const uint8_t* x_dev, int nb, int h, int w, int c,
                                   int32_t zp_a, const q8g_packed_b* pw, int32_t* y_dev,
                                   int img_begin, int img_end, void* stream);
+/* host views (the reference calling convention, engine.hpp:59-62): images of
+ * x_host / y_host are staged through the device in chunks whose copies
+ * overlap the previous chunk's convolution; synchronous */
+int q8g_conv3x3_u8s8_nhwc_host(const uint8_t* x_host, int nb, int h, int w, int c,
+                               const q8g_packed_b* pw, const q8g_epilogue* ep, uint8_t* y_host,
+                               int img_begin, int img_end, void* stream);
 
 /* ---- depthwise 3x3, stride 1, pad 1, NHWC (new) ----
  * w_host: [3][3][c] s8.  Requant params are per channel (k_total = 9). */
@@ -199,6 +211,10 @@ int q8g_dw_filter_free(q8g_dw_filter* f);
 int q8g_dwconv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
                             const q8g_dw_filter* f, uint8_t* y_dev, int img_begin, int img_end,
                             void* stream);
+/* host views, chunked and overlapped like q8g_conv3x3_u8s8_nhwc_host */
+int q8g_dwconv3x3_u8s8_nhwc_host(const uint8_t* x_host, int nb, int h, int w, int c,
+                                 const q8g_dw_filter* f, uint8_t* y_host, int img_begin, int img_end,
+                                 void* stream);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,7 @@ _SIGS = [
     ("q8g_launch_count", C.c_uint64, []),
     ("q8g_launch_stats", _I, [C.POINTER(C.c_uint64), _I]),
     ("q8g_debug_tc_trace", _I, [C.POINTER(C.c_uint64), _I]),
+    ("q8g_debug_kernel_clock", _I, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("q8g_blocking_defaults", _I, [C.POINTER(Blocking)]),
     ("q8g_blocking_validate", _I, [C.POINTER(Blocking)]),
     ("q8g_select_blocking", _I, [_I, _I, _I, C.POINTER(Blocking), C.POINTER(Blocking)]),
@@ -94,9 +95,11 @@ _SIGS = [
     ("q8g_gemm_u8s8_raw_i32_host", _I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _P]),
     ("q8g_conv3x3_u8s8_nhwc", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _P]),
     ("q8g_conv3x3_u8s8_nhwc_raw_i32", _I, [_P, _I, _I, _I, _I, C.c_int32, _P, _P, _I, _I, _P]),
+    ("q8g_conv3x3_u8s8_nhwc_host", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _P]),
     ("q8g_dw_filter_create", _I, [_P, _I, C.POINTER(RequantParamsC), _I, C.POINTER(_P)]),
     ("q8g_dw_filter_free", _I, [_P]),
     ("q8g_dwconv3x3_u8s8_nhwc", _I, [_P, _I, _I, _I, _I, _P, _P, _I, _I, _P]),
+    ("q8g_dwconv3x3_u8s8_nhwc_host", _I, [_P, _I, _I, _I, _I, _P, _P, _I, _I, _P]),
     ("q8g_split_outliers", _I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _I, C.POINTER(_I)]),
     ("q8g_sparse_csc_create", _I, [_P, _P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
     ("q8g_sparse_csc_free", _I, [_P]),

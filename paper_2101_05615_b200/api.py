@@ -98,7 +98,7 @@ def _is_dev(x) -> bool:
 
 
 def _ld(x) -> int:
-    if _is_dev(x):
+    if torch is not None and isinstance(x, torch.Tensor):
         if x.dim() != 2 or x.stride(1) != 1:
             raise InvalidArgument(_lib.Q8G_EINVAL, "matrix views must be row-major with unit column stride")
         return x.stride(0)
@@ -108,7 +108,7 @@ def _ld(x) -> int:
 
 
 def _ptr(x) -> int:
-    return x.data_ptr() if _is_dev(x) else x.ctypes.data
+    return x.data_ptr() if torch is not None and isinstance(x, torch.Tensor) else x.ctypes.data
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -568,6 +568,13 @@ def _execute_general(a, pw: PackedWeight, out, pipeline: OutputPipeline, r0: int
 
 # ---------------------------------------------------------------- conv 3x3
 
+def _host_contig(*arrays) -> None:
+    for a in arrays:
+        contiguous = a.is_contiguous() if isinstance(a, torch.Tensor) else a.flags["C_CONTIGUOUS"]
+        if not contiguous:
+            raise InvalidArgument(_lib.Q8G_EINVAL, "host views of NHWC tensors must be contiguous")
+
+
 def prepack_conv3x3_weights(w, device: int = 0) -> PackedWeight:
     """w: [3][3][C][OC] int8 -> packed K=9C x N=OC matrix."""
     if _is_dev(w):
@@ -586,6 +593,14 @@ def execute_conv3x3(x, pw: PackedWeight, out, pipeline: OutputPipeline, zp_a: Op
         raise InvalidArgument(_lib.Q8G_EINVAL, "conv3x3: output must be [N,H,W,OC]")
     image_end = nb if image_end is None else image_end
     lib = load()
+    if not _is_dev(x):
+        # host views (the reference convention): chunked, copies overlapped with the convolution
+        if _is_dev(out) or pipeline.writer() is not Requantize:
+            raise InvalidArgument(_lib.Q8G_EINVAL, "conv3x3: host views need host x and out and the Requantize writer")
+        _host_contig(x, out)
+        check(lib.q8g_conv3x3_u8s8_nhwc_host(_ptr(x), nb, h, w, c, pw.handle, pipeline.epilogue(pw), _ptr(out),
+                                             image_begin, image_end, _stream_ptr(stream)))
+        return
     if pipeline.writer() is WriteRawI32:
         zp_a = 0 if zp_a is None else int(zp_a)
         check(lib.q8g_conv3x3_u8s8_nhwc_raw_i32(x.data_ptr(), nb, h, w, c, zp_a, pw.handle, out.data_ptr(),
@@ -640,5 +655,12 @@ def execute_dwconv3x3(x, filt: DepthwiseFilter, out, image_begin: int = 0, image
     if out.shape != x.shape:
         raise InvalidArgument(_lib.Q8G_EINVAL, "dwconv3x3: output must be [N,H,W,C]")
     image_end = nb if image_end is None else image_end
+    if not _is_dev(x):
+        if _is_dev(out):
+            raise InvalidArgument(_lib.Q8G_EINVAL, "dwconv3x3: x and out must both be device or both host views")
+        _host_contig(x, out)
+        check(load().q8g_dwconv3x3_u8s8_nhwc_host(_ptr(x), nb, h, w, c, filt._h, _ptr(out), image_begin, image_end,
+                                                  _stream_ptr(stream)))
+        return
     check(load().q8g_dwconv3x3_u8s8_nhwc(x.data_ptr(), nb, h, w, c, filt._h, out.data_ptr(), image_begin,
                                          image_end, _stream_ptr(stream)))

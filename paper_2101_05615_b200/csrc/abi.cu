@@ -7,7 +7,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -121,6 +123,15 @@ extern "C" {
 const char* q8g_last_error(void) { return g_last_error.c_str(); }
 int q8g_version(void) { return 1; }
 uint64_t q8g_launch_count(void) { return g_launches.load(); }
+
+int q8g_debug_kernel_clock(uint64_t* cycles, uint64_t* ns) {
+    if (!cycles || !ns) return fail(Q8G_EINVAL, "null argument");
+    unsigned long long c = 0, t = 0;
+    if (tc2w_last_clock(&c, &t)) return fail(Q8G_ECUDA, "kernel clock readback failed");
+    *cycles = c;
+    *ns = t;
+    return Q8G_OK;
+}
 
 int q8g_debug_tc_trace(uint64_t* out, int max_ctas) {
     if (!out || max_ctas < 1) return 0;
@@ -690,6 +701,102 @@ int q8g_gemm_u8s8_pipeline_host(const uint8_t* a_host, int m, int k, int lda, co
 
 }  // extern "C"
 
+// Chunked host-view pipeline (large host-view calls): the inputs are split
+// into chunks of `chunk` units (GEMM rows or images); chunk i's H2D copy, its
+// compute and chunk i-1's D2H copy overlap on three streams (PCIe is full
+// duplex), so a call costs about max(H2D, D2H) + one chunk instead of
+// H2D + compute + D2H.  Per-device grow-only staging, calls serialised per
+// device, synchronous for the caller.
+namespace {
+constexpr int kMaxChunks = 64;
+struct HostPipe {
+    std::mutex mu;
+    uint8_t* in = nullptr;
+    uint8_t* out = nullptr;
+    size_t in_bytes = 0, out_bytes = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
+    cudaEvent_t done = nullptr;
+};
+HostPipe g_host_pipe[64];
+
+struct HostPipeSpec {
+    const uint8_t* in_host;
+    size_t in_pitch, in_width, in_dpitch;    // bytes per unit row: host pitch, copied bytes, device pitch
+    uint8_t* out_host;
+    size_t out_pitch, out_width, out_dpitch;
+    int units, chunk;
+};
+
+template <class F>
+int run_host_pipeline(int device, cudaStream_t s, const HostPipeSpec& sp, F compute) {
+    HostPipe& hp = g_host_pipe[device & 63];
+    std::lock_guard<std::mutex> lock(hp.mu);
+    cudaError_t e;
+    const size_t need_in = sp.in_dpitch * (size_t)sp.units, need_out = sp.out_dpitch * (size_t)sp.units;
+    if (hp.in_bytes < need_in) {
+        if (hp.in) cudaFree(hp.in);
+        hp.in = nullptr;
+        hp.in_bytes = 0;
+        if ((e = cudaMalloc(&hp.in, need_in)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(host pipeline input)");
+        hp.in_bytes = need_in;
+    }
+    if (hp.out_bytes < need_out) {
+        if (hp.out) cudaFree(hp.out);
+        hp.out = nullptr;
+        hp.out_bytes = 0;
+        if ((e = cudaMalloc(&hp.out, need_out)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(host pipeline output)");
+        hp.out_bytes = need_out;
+    }
+    if (!hp.h2d) {
+        if ((e = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&hp.done, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "host pipeline streams");
+        for (int i = 0; i < kMaxChunks; ++i)
+            if ((e = cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&hp.ev_out[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "host pipeline events");
+    }
+    int chunk = sp.chunk < 1 ? 1 : sp.chunk;
+    if ((sp.units + chunk - 1) / chunk > kMaxChunks) chunk = (sp.units + kMaxChunks - 1) / kMaxChunks;
+    // the staging buffers may still be read by work the caller queued on s
+    // before this call (a previous call is complete: calls are synchronous)
+    if ((e = cudaEventRecord(hp.done, s)) != cudaSuccess || (e = cudaStreamWaitEvent(hp.h2d, hp.done, 0)) != cudaSuccess)
+        return cuda_fail(e, "host pipeline ordering");
+    int rc = Q8G_OK, i = 0;
+    for (int u0 = 0; u0 < sp.units && rc == Q8G_OK; u0 += chunk, ++i) {
+        const int u1 = u0 + chunk < sp.units ? u0 + chunk : sp.units;
+        const size_t n = (size_t)(u1 - u0);
+        uint8_t* din = hp.in + sp.in_dpitch * u0;
+        uint8_t* dout = hp.out + sp.out_dpitch * u0;
+        e = cudaMemcpy2DAsync(din, sp.in_dpitch, sp.in_host + sp.in_pitch * u0, sp.in_pitch, sp.in_width, n,
+                              cudaMemcpyHostToDevice, hp.h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(hp.ev_in[i], hp.h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, hp.ev_in[i], 0);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "host pipeline H2D");
+            break;
+        }
+        rc = compute(u0, u1, din, dout);
+        if (rc) break;
+        e = cudaEventRecord(hp.ev_out[i], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.ev_out[i], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(sp.out_host + sp.out_pitch * u0, sp.out_pitch, dout, sp.out_dpitch, sp.out_width, n,
+                                  cudaMemcpyDeviceToHost, hp.d2h);
+        if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline D2H");
+    }
+    // drain every stream before the staging can be reused (also on error)
+    cudaError_t e1 = cudaEventRecord(hp.done, hp.d2h);
+    if (e1 == cudaSuccess) e1 = cudaEventSynchronize(hp.done);
+    cudaStreamSynchronize(hp.h2d);
+    cudaStreamSynchronize(s);
+    if (!rc && e1 != cudaSuccess) rc = cuda_fail(e1, "host pipeline completion");
+    return rc;
+}
+}  // namespace
+
 template <typename OutT>
 static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_packed_b* pb,
                      const q8g_epilogue* ep, OutT* c_host, int ldc, int row_begin, int row_end,
@@ -703,6 +810,17 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
     if (rows == 0) return Q8G_OK;
     DeviceGuard dg(pb->device);
     const int lda_d = round_up_i(k, 16), ldc_d = pb->n;
+    if (rows >= 4096) {
+        // large stripes: chunks of >= 1024 rows (multiples of the 256-row
+        // pair tile), copies overlapped with the GEMM of the previous chunk
+        HostPipeSpec sp{a_host + (size_t)row_begin * lda, (size_t)lda, (size_t)k, (size_t)lda_d,
+                        reinterpret_cast<uint8_t*>(c_host + (size_t)row_begin * ldc), sizeof(OutT) * ldc,
+                        sizeof(OutT) * pb->n, sizeof(OutT) * ldc_d, rows, round_up_i(std::max(1024, rows / 16), 256)};
+        return run_host_pipeline(pb->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
+            return gemm_common(din, u1 - u0, k, lda_d, pb, raw ? nullptr : ep, nullptr, dout, ldc_d, 0, u1 - u0,
+                               nullptr, s, raw);
+        });
+    }
     // grow-only per-device staging buffers; host-view calls are synchronous
     // and serialised per device by this lock.  A is copied on a separate
     // stream followed by a copy of the call's epoch into `flag`: the
@@ -1011,6 +1129,50 @@ int q8g_dwconv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
                                      y_dev + img_begin * img, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "dwconv3x3 launch");
     return Q8G_OK;
+}
+
+
+/* host views: images [img_begin, img_end) of x_host are staged through the
+ * device in chunks whose copies overlap the previous chunk's convolution;
+ * synchronous (the reference calling convention) */
+int q8g_conv3x3_u8s8_nhwc_host(const uint8_t* x_host, int nb, int h, int w, int c, const q8g_packed_b* pw,
+                               const q8g_epilogue* ep, uint8_t* y_host, int img_begin, int img_end, void* stream) {
+    if (!pw || !ep || !x_host || !y_host) return fail(Q8G_EINVAL, "conv3x3: null argument");
+    if (nb < 1 || h < 1 || w < 1 || c < 1) return fail(Q8G_EINVAL, "conv3x3: dimensions must be >= 1");
+    if (img_begin < 0 || img_end > nb || img_begin > img_end)
+        return fail(Q8G_EINVAL, "conv3x3: image range out of bounds");
+    if (img_begin == img_end) return Q8G_OK;
+    DeviceGuard dg(pw->device);
+    const size_t xi = (size_t)h * w * c, yi = (size_t)h * w * pw->n;
+    const int imgs = img_end - img_begin;
+    HostPipeSpec sp{x_host + xi * img_begin, xi, xi, xi, y_host + yi * img_begin, yi, yi, yi, imgs,
+                    std::max(1, (imgs + 7) / 8)};
+    const cudaStream_t s = (cudaStream_t)stream;
+    return run_host_pipeline(pw->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
+        (void)u0;
+        return conv_common(din, u1 - u0, h, w, c, ep->zp_a, pw, ep, dout, 0, u1 - u0, s, false);
+    });
+}
+
+int q8g_dwconv3x3_u8s8_nhwc_host(const uint8_t* x_host, int nb, int h, int w, int c, const q8g_dw_filter* f,
+                                 uint8_t* y_host, int img_begin, int img_end, void* stream) {
+    if (!f || !x_host || !y_host) return fail(Q8G_EINVAL, "dwconv3x3: null argument");
+    if (nb < 1 || h < 1 || w < 1 || c < 1) return fail(Q8G_EINVAL, "dwconv3x3: dimensions must be >= 1");
+    if (c != f->c) return fail(Q8G_EINVAL, "dwconv3x3: channel count does not match the filter");
+    if (img_begin < 0 || img_end > nb || img_begin > img_end)
+        return fail(Q8G_EINVAL, "dwconv3x3: image range out of bounds");
+    if (img_begin == img_end) return Q8G_OK;
+    DeviceGuard dg(f->device);
+    const size_t img = (size_t)h * w * c;
+    const int imgs = img_end - img_begin;
+    HostPipeSpec sp{x_host + img * img_begin, img, img, img, y_host + img * img_begin, img, img, img, imgs,
+                    std::max(1, (imgs + 15) / 16)};
+    const cudaStream_t s = (cudaStream_t)stream;
+    return run_host_pipeline(f->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
+        (void)u0;
+        const cudaError_t e = launch_dwconv3x3(din, u1 - u0, h, w, c, f, dout, s);
+        return e == cudaSuccess ? Q8G_OK : cuda_fail(e, "dwconv3x3 launch");
+    });
 }
 
 }  // extern "C"

@@ -118,13 +118,23 @@ __device__ __forceinline__ TileRange tile_range(const Tc2wParams& p, int group, 
     return {group, total, groups};
 }
 
+// CTA 0's SM clock64 and globaltimer at entry / exit of the most recent
+// launch (always recorded: two 16-byte stores per launch), read back by
+// q8g_debug_kernel_clock: the SM clock the launch actually ran at (NVML
+// reports the clock target, not the power-limited effective clock)
+__device__ unsigned long long g_tc2w_clock[4];
+
 __device__ __forceinline__ void tw_clk(const Tc2wParams& p, int end) {
-    if (p.trace && blockIdx.x == 0) {
+    if (blockIdx.x == 0) {
         unsigned long long t, c;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
-        p.trace[10200 + end] = c;
-        p.trace[10202 + end] = t;
+        g_tc2w_clock[end] = c;
+        g_tc2w_clock[2 + end] = t;
+        if (p.trace) {
+            p.trace[10200 + end] = c;
+            p.trace[10202 + end] = t;
+        }
     }
 }
 // CTA 0, per tile ti < 16: [9216 + 8 * ti + k] (tools/tc2w_tiles.py): MMA
@@ -711,6 +721,15 @@ cudaError_t launch_tc2w(const GemmArgs& g, cudaStream_t s) {
 }
 
 }  // namespace
+
+// clock64 cycles and globaltimer ns of CTA 0 of the last 256 x 512 pair-kernel launch
+int tc2w_last_clock(unsigned long long* cycles, unsigned long long* ns) {
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (cudaMemcpyFromSymbol(h, g_tc2w_clock, sizeof(h)) != cudaSuccess) return -1;
+    *cycles = h[1] - h[0];
+    *ns = h[3] - h[2];
+    return 0;
+}
 
 // the 512-column pair tile needs N padded to 512 (np % 512 == 0); Q8G_TC2W=0
 // falls back to the 256 x 256 pair kernel (gemm_tc2.cu)

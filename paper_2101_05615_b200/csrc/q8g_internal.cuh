@@ -214,6 +214,7 @@ cudaError_t launch_post(int writer, const int32_t* acc, int ldacc, const uint8_t
                         int ldc, cudaStream_t s);
 cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s);
 bool tc2w_supported(const GemmArgs& g);
+int tc2w_last_clock(unsigned long long* cycles, unsigned long long* ns);
 cudaError_t launch_gemm_tc2w(const GemmArgs& g, cudaStream_t s);
 int tc_trace_copy(unsigned long long* out, int max_ctas);
 

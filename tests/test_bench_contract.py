@@ -20,7 +20,7 @@ def run_bench(*args, env_extra=None, timeout=300):
     return r.returncode, r.stdout, r.stderr
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C3", "C4"])
+@pytest.mark.parametrize("cfg", ["C2", "C1", "C3", "C4"])
 def test_reference_arm_line(cfg):
     if not (ROOT / "oracle" / "_ref").exists() and cfg != "C4":
         pytest.skip("oracle/_ref not built")
@@ -35,6 +35,18 @@ def test_reference_arm_line(cfg):
     assert d["e2e"]["value"] == d["value"] == d["cpu_baseline"]["value"]
     assert d["cpu_baseline"]["kind"] == ("port" if cfg == "C4" else "reference")
     assert d["cpu_baseline"]["cores"] >= 1
+    # the same workload identity as our arm's line (the driver compares them)
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert d["config"] == bench.config_dict(cfg, 1)
+    assert d["ms_per_step"] > 0
+
+
+def test_default_config_is_the_c2_headline():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert bench.HEADLINE == "C2" and bench.BOUND["C2"] == "tensor"
+    assert bench.config_dict("C2", 8)["M"] == 16384
 
 
 def test_reference_arm_other_ranks_silent():

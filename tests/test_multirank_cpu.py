@@ -6,8 +6,11 @@
   stands in for the GPU kernel), the stripes are gathered and must equal the
   single-process result bit for bit, ragged last stripe and empty ranks
   included -- the path shards with no data-path collective;
-- timing: bench.max_over_ranks takes the element-wise max over ranks and
-  bench.whole_job_tops aggregates all ranks' work (weak scaling).
+- strong scaling (bench.py --gpus N): the C2 row stripes and the C3 / C4
+  image ranges of the ranks cover the whole configuration exactly once, and
+  the headline value is the configuration's total ops over the
+  max-over-ranks step time;
+- timing: bench.max_over_ranks takes the element-wise max over ranks.
 """
 import os
 import socket
@@ -92,8 +95,20 @@ def test_row_sharding_two_ranks_matches_single_process(m, world):
     assert t == [float(world), 10.0, 0.5 * world]
 
 
-def test_whole_job_value_is_weak_scaling_aggregate():
+def test_strong_scaling_partitions_cover_each_config_once():
     import bench
-    one = bench.whole_job_tops(128, 4096, 4096, 1, 0.01)
-    assert bench.whole_job_tops(128, 4096, 4096, 8, 0.01) == pytest.approx(8 * one)
-    assert one == pytest.approx(2 * 128 * 4096 * 4096 / 1e-5 / 1e12)
+    for world in (1, 2, 4, 8, 3):
+        m = bench.GEMM_CONFIGS["C2"][0]
+        stripes = [bench.gemm_rows(m, r, world) for r in range(world)]
+        assert stripes[0][0] == 0 and stripes[-1][1] == m
+        assert all(a[1] == b[0] for a, b in zip(stripes, stripes[1:]))
+        assert max(b - a for a, b in stripes) - min(b - a for a, b in stripes) <= 128  # balanced 128-row blocks
+        for cfg in ("C3", "C4"):
+            nb = bench.CONV_CONFIGS[cfg][0]
+            imgs = [bench.image_range(nb, r, world) for r in range(world)]
+            assert imgs[0][0] == 0 and imgs[-1][1] == nb
+            assert all(a[1] == b[0] for a, b in zip(imgs, imgs[1:]))
+    # value = the whole configuration's ops over the slowest rank's step time
+    ops = bench.gemm_ops("C2")
+    assert ops == 2.0 * 16384 * 4096 * 4096
+    assert bench.whole_job_tops(ops, 0.2) == pytest.approx(ops / 0.2e-3 / 1e12)

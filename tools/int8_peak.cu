@@ -3,24 +3,49 @@
 // SM issues back-to-back tcgen05.mma.kind::i8 (M=128, N=256, K=32, A u8 /
 // B s8 from SWIZZLE_128B smem, s32 accumulators in TMEM) and the whole grid is
 // timed with CUDA events.  Burst = best of short runs; sustained = one ~2 s
-// run.  Prints one JSON line.
+// run.  Two operand patterns:
+//   "hash"   : the round-1 pattern, word i = i * 2654435761 over 48 KB (the
+//              same 4 K-slices of A and B re-read in turn);
+//   "random" : 192 KB of xorshift bytes per CTA, 16 A and 16 B K-slices
+//              combined in a rotating order -- the toggle activity of real
+//              uniform u8 / s8 data, which sets the clock under the 1 kW cap.
+// The in-kernel clock64 / globaltimer ratio of CTA 0 gives the SM clock the
+// run achieved.  Prints one JSON line.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_2101_05615_b200/csrc int8_peak.cu -o int8_peak
+#include <algorithm>
 #include <cstdio>
 #include <vector>
-#include <algorithm>
 
 #include "ptx.cuh"
 
 using namespace q8g;
 
-__global__ void __launch_bounds__(128, 1) peak_kernel(long long iters, unsigned long long* sink) {
+constexpr int kSmem = 192 * 1024 + 1024;
+
+__global__ void __launch_bounds__(128, 1) peak_kernel(long long iters, int random, unsigned long long* sink,
+                                                      unsigned long long* clk) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tptr;
     const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* sm = smem_raw + (base - ptx::smem_u32(smem_raw));
-    for (int i = threadIdx.x; i < 48 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = i * 2654435761u;
+    unsigned long long c0 = 0, t0 = 0;
+    if (threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0));
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    }
+    if (random) {
+        uint32_t x = 0x9E3779B9u * (blockIdx.x * 128 + threadIdx.x + 1);
+        for (int i = threadIdx.x; i < 192 * 1024 / 4; i += blockDim.x) {
+            x ^= x << 13;
+            x ^= x >> 17;
+            x ^= x << 5;
+            reinterpret_cast<uint32_t*>(sm)[i] = x;
+        }
+    } else {
+        for (int i = threadIdx.x; i < 48 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = i * 2654435761u;
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         ptx::mbar_init(ptx::smem_u32(&bar), 1);
@@ -32,11 +57,23 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(long long iters, unsigned 
     ptx::tc_fence_after();
     const uint32_t tmem = tptr;
     constexpr uint32_t idesc = ptx::idesc_u8s8_s32<128, 256>();
-    const uint64_t ad = ptx::sw128_kmajor_desc(base), bd = ptx::sw128_kmajor_desc(base + 16384);
     if (threadIdx.x < 32) {
         if (ptx::elect_one()) {
-            for (long long i = 0; i < iters; ++i)
-                ptx::mma_i8(tmem + (uint32_t)((i & 1) * 256), ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i > 1);
+            if (random) {
+                // A: 4 blocks of 128 rows x 128 B (64 KB), B: 4 blocks of 256 rows x 128 B (128 KB);
+                // 4 K-slices of 32 B per block
+                const uint64_t ad0 = ptx::sw128_kmajor_desc(base), bd0 = ptx::sw128_kmajor_desc(base + 65536);
+                for (long long i = 0; i < iters; ++i) {
+                    const uint32_t ia = (uint32_t)i & 15u, ib = ((uint32_t)i * 7u + ((uint32_t)i >> 4)) & 15u;
+                    const uint64_t ad = ad0 + (uint64_t)((ia >> 2) * (16384 >> 4)) + 2 * (ia & 3);
+                    const uint64_t bd = bd0 + (uint64_t)((ib >> 2) * (32768 >> 4)) + 2 * (ib & 3);
+                    ptx::mma_i8(tmem + (uint32_t)((i & 1) * 256), ad, bd, idesc, i > 1);
+                }
+            } else {
+                const uint64_t ad = ptx::sw128_kmajor_desc(base), bd = ptx::sw128_kmajor_desc(base + 16384);
+                for (long long i = 0; i < iters; ++i)
+                    ptx::mma_i8(tmem + (uint32_t)((i & 1) * 256), ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i > 1);
+            }
             ptx::tc_commit(ptx::smem_u32(&bar));
         }
         __syncwarp();
@@ -52,36 +89,59 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(long long iters, unsigned 
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x < 32) ptx::tmem_dealloc<512>(tmem);
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long c1, t1;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1));
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        clk[0] = c1 - c0;
+        clk[1] = t1 - t0;
+    }
 }
 
-static double run(int sms, long long iters) {
-    unsigned long long* sink;
+struct Run {
+    double tops, mhz;
+};
+
+static Run run(int sms, long long iters, int random) {
+    unsigned long long *sink, *clk;
     cudaMalloc(&sink, 8);
+    cudaMalloc(&clk, 16);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    peak_kernel<<<sms, 128, 64 * 1024>>>(iters, sink);
+    peak_kernel<<<sms, 128, kSmem>>>(iters, random, sink, clk);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
+    unsigned long long hc[2] = {0, 1};
+    cudaMemcpy(hc, clk, 16, cudaMemcpyDeviceToHost);
     cudaFree(sink);
-    return (double)sms * iters * 2.0 * 128 * 256 * 32 / (ms * 1e-3) / 1e12;
+    cudaFree(clk);
+    return {(double)sms * iters * 2.0 * 128 * 256 * 32 / (ms * 1e-3) / 1e12, (double)hc[0] / (double)hc[1] * 1e3};
 }
 
 int main() {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaFuncSetAttribute(peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    run(sms, 20000);  // warm-up
-    std::vector<double> burst;
-    for (int r = 0; r < 10; ++r) burst.push_back(run(sms, 100000));  // ~7 ms each at peak
-    const double best = *std::max_element(burst.begin(), burst.end());
-    const double sustained = run(sms, 30000000);  // ~2 s
+    cudaFuncSetAttribute(peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    run(sms, 20000, 0);  // warm-up
+    Run best[2] = {{0, 0}, {0, 0}};
+    for (int mode = 0; mode < 2; ++mode)
+        for (int r = 0; r < 10; ++r) {  // ~7 ms each at peak
+            const Run x = run(sms, 100000, mode);
+            if (x.tops > best[mode].tops) best[mode] = x;
+        }
+    const Run sustained = run(sms, 30000000, 0);  // ~2 s
+    const Run sustained_rnd = run(sms, 20000000, 1);
     cudaError_t e = cudaGetLastError();
-    std::printf("{\"int8_tops_burst\": %.1f, \"int8_tops_sustained\": %.1f, \"sms\": %d, \"shape\": "
-                "\"tcgen05.mma.kind::i8 M128 N256 K32, SS (SW128), back-to-back, 1 CTA/SM\", \"error\": \"%s\"}\n",
-                best, sustained, sms, cudaGetErrorString(e));
+    std::printf("{\"int8_tops_burst\": %.1f, \"int8_tops_burst_mhz\": %.0f, \"int8_tops_sustained\": %.1f, "
+                "\"int8_tops_sustained_mhz\": %.0f, \"int8_tops_burst_random\": %.1f, \"int8_tops_burst_random_mhz\": "
+                "%.0f, \"int8_tops_sustained_random\": %.1f, \"int8_tops_sustained_random_mhz\": %.0f, \"sms\": %d, "
+                "\"shape\": \"tcgen05.mma.kind::i8 M128 N256 K32, SS (SW128), back-to-back, 1 CTA/SM\", "
+                "\"error\": \"%s\"}\n",
+                best[0].tops, best[0].mhz, sustained.tops, sustained.mhz, best[1].tops, best[1].mhz, sustained_rnd.tops,
+                sustained_rnd.mhz, sms, cudaGetErrorString(e));
     return e == cudaSuccess ? 0 : 1;
 }
