@@ -193,6 +193,11 @@ int q8g_gemm_u8s8_pipeline_host(const uint8_t* a_host, int m, int k, int lda, co
 int q8g_conv3x3_u8s8_nhwc(const uint8_t* x_dev, int nb, int h, int w, int c,
                           const q8g_packed_b* pw, const q8g_epilogue* ep, uint8_t* y_dev,
                           int img_begin, int img_end, void* stream);
+/* build, once and synchronously, the derived tensor-core operand image of a
+ * conv weight for c input channels (pw->k == 9c); the first conv call does it
+ * otherwise (and must then not be inside a stream capture).  After it the
+ * weight is used read-only by any number of concurrent streams. */
+int q8g_conv3x3_prepare(const q8g_packed_b* pw, int c, void* stream);
 int q8g_conv3x3_u8s8_nhwc_raw_i32(const uint8_t* x_dev, int nb, int h, int w, int c,
                                   int32_t zp_a, const q8g_packed_b* pw, int32_t* y_dev,
                                   int img_begin, int img_end, void* stream);

@@ -531,9 +531,12 @@ void execute_gemm(DeviceView<const uint8_t> a, const PackedWeight& pw, DeviceVie
 
 // ------------------------------------------------------------------ conv / depthwise (new entry points)
 
-// weights [3][3][C][OC] int8 (host) -> packed K = 9C x N = OC
+// weights [3][3][C][OC] int8 (host) -> packed K = 9C x N = OC, with the
+// tensor-core operand image built eagerly: immutable and shareable from here on
 inline PackedWeight prepack_conv3x3_weights(const int8_t* w_host, int c, int oc, int device = 0) {
-    return prepack_weights(MatrixView<const int8_t>{w_host, 9 * c, oc, oc}, BlockingParams::defaults(), device);
+    PackedWeight pw = prepack_weights(MatrixView<const int8_t>{w_host, 9 * c, oc, oc}, BlockingParams::defaults(), device);
+    check(q8g_conv3x3_prepare(pw.handle(), c, nullptr));
+    return pw;
 }
 
 // NHWC device tensors, stride 1, pad 1 with zp_a; images [img_begin, img_end)
@@ -542,6 +545,13 @@ inline void execute_conv3x3(const uint8_t* x_dev, int nb, int h, int w, int c, c
                             void* stream = nullptr) {
     check(q8g_conv3x3_u8s8_nhwc(x_dev, nb, h, w, c, pw.handle(), pipeline.epilogue(pw), y_dev, img_begin, img_end,
                                 stream));
+}
+// host views (the reference calling convention): chunked, copies overlapped, synchronous
+inline void execute_conv3x3_host(const uint8_t* x_host, int nb, int h, int w, int c, const PackedWeight& pw,
+                                 const OutputPipeline& pipeline, uint8_t* y_host, int img_begin, int img_end,
+                                 void* stream = nullptr) {
+    check(q8g_conv3x3_u8s8_nhwc_host(x_host, nb, h, w, c, pw.handle(), pipeline.epilogue(pw), y_host, img_begin,
+                                     img_end, stream));
 }
 
 class DepthwiseFilter {
@@ -572,6 +582,10 @@ private:
 inline void execute_dwconv3x3(const uint8_t* x_dev, int nb, int h, int w, int c, const DepthwiseFilter& f,
                               uint8_t* y_dev, int img_begin, int img_end, void* stream = nullptr) {
     check(q8g_dwconv3x3_u8s8_nhwc(x_dev, nb, h, w, c, f.handle(), y_dev, img_begin, img_end, stream));
+}
+inline void execute_dwconv3x3_host(const uint8_t* x_host, int nb, int h, int w, int c, const DepthwiseFilter& f,
+                                   uint8_t* y_host, int img_begin, int img_end, void* stream = nullptr) {
+    check(q8g_dwconv3x3_u8s8_nhwc_host(x_host, nb, h, w, c, f.handle(), y_host, img_begin, img_end, stream));
 }
 
 }  // namespace q8gemm_b200

@@ -95,6 +95,7 @@ _SIGS = [
     ("q8g_gemm_u8s8_raw_i32_host", _I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _P]),
     ("q8g_conv3x3_u8s8_nhwc", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _P]),
     ("q8g_conv3x3_u8s8_nhwc_raw_i32", _I, [_P, _I, _I, _I, _I, C.c_int32, _P, _P, _I, _I, _P]),
+    ("q8g_conv3x3_prepare", _I, [_P, _I, _P]),
     ("q8g_conv3x3_u8s8_nhwc_host", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _P]),
     ("q8g_dw_filter_create", _I, [_P, _I, C.POINTER(RequantParamsC), _I, C.POINTER(_P)]),
     ("q8g_dw_filter_free", _I, [_P]),

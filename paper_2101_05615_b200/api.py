@@ -365,6 +365,20 @@ class OutputPipeline:
                 acc = b if acc is None else acc + b
         return None if acc is None else acc.astype(np.int32)
 
+    def bias_add_device(self, device):
+        """The summed BiasAdd stages as a device tensor, cached on the pipeline
+        so it outlives the (asynchronous) launches that read it -- a temporary
+        freed at return could be recycled by the caching allocator while a
+        kernel on another stream still reads it."""
+        ba = self.bias_add()
+        if ba is None:
+            return None
+        cache = self.__dict__.setdefault("_bias_dev", {})
+        key = torch.device(device).index
+        if key not in cache:
+            cache[key] = torch.from_numpy(ba).to(device)
+        return cache[key]
+
     def sparse(self) -> Optional[SparseWeightCSC]:
         for s in self.stages:
             if isinstance(s, SpMDMAdd):
@@ -502,7 +516,7 @@ def execute_gemm(a, pw: PackedWeight, out, pipeline: OutputPipeline,
         if dev:
             bdev = None
             if ba is not None:
-                bdev = torch.from_numpy(ba).to(a.device)
+                bdev = pipeline.bias_add_device(a.device)
             check(lib.q8g_gemm_u8s8_raw_i32(a.data_ptr(), m, k, lda, pw.handle,
                                             None if bdev is None else bdev.data_ptr(), out.data_ptr(), ldc,
                                             r0, r1, cache_h, _stream_ptr(stream)))
@@ -549,10 +563,8 @@ def _execute_general(a, pw: PackedWeight, out, pipeline: OutputPipeline, r0: int
         pa.ep = pipeline.epilogue(pw)  # folds BiasAdd into the table
     else:
         pa.writer = _lib.Q8G_WRITE_RAW_I32 if w is WriteRawI32 else _lib.Q8G_WRITE_DEQUANT_F32
-        ba = pipeline.bias_add()
-        if ba is not None:
-            bdev = torch.from_numpy(ba).to(a_d.device)
-            keep.append(bdev)
+        bdev = pipeline.bias_add_device(a_d.device)
+        if bdev is not None:
             pa.bias_add_dev = bdev.data_ptr()
         if w is WriteDequantF32:
             cp = pipeline.stages[-1].c_params
@@ -576,11 +588,14 @@ def _host_contig(*arrays) -> None:
 
 
 def prepack_conv3x3_weights(w, device: int = 0) -> PackedWeight:
-    """w: [3][3][C][OC] int8 -> packed K=9C x N=OC matrix."""
-    if _is_dev(w):
-        return prepack_weights(w.reshape(-1, w.shape[-1]), device=device)
-    w = np.asarray(w)
-    return prepack_weights(w.reshape(-1, w.shape[-1]), device=device)
+    """w: [3][3][C][OC] int8 -> packed K=9C x N=OC matrix,
+    with the tensor-core operand image built eagerly (q8g_conv3x3_prepare) so
+    the weight is immutable from here on."""
+    if not _is_dev(w):
+        w = np.asarray(w)
+    pw = prepack_weights(w.reshape(-1, w.shape[-1]), device=device)
+    check(load().q8g_conv3x3_prepare(pw.handle, int(w.shape[2]), None))
+    return pw
 
 
 def execute_conv3x3(x, pw: PackedWeight, out, pipeline: OutputPipeline, zp_a: Optional[int] = None,

@@ -262,9 +262,10 @@ int q8g_packed_b_replicate(const q8g_packed_b* src, int device, q8g_packed_b** o
     pb->device = device;
     pb->data = nullptr;
     pb->colsum_dev = nullptr;
-    pb->conv_img = nullptr;  // rebuilt lazily on the replica's device
-    pb->conv_img_c = 0;
-    pb->conv_img_bytes = 0;
+    for (int i = 0; i < 3; ++i) {  // rebuilt on the replica's device
+        pb->conv_img[i] = nullptr;
+        pb->conv_img_ready[i] = 0;
+    }
     pb->colsum_host = (int32_t*)malloc(sizeof(int32_t) * src->np);
     memcpy(pb->colsum_host, src->colsum_host, sizeof(int32_t) * src->np);
     cudaError_t e;
@@ -330,7 +331,8 @@ int q8g_free_packed_b(q8g_packed_b* pb) {
     DeviceGuard dg(pb->device);
     if (pb->data) cudaFree(pb->data);
     if (pb->colsum_dev) cudaFree(pb->colsum_dev);
-    if (pb->conv_img) cudaFree(pb->conv_img);
+    for (int i = 0; i < 3; ++i)
+        if (pb->conv_img[i]) cudaFree(pb->conv_img[i]);
     free(pb->colsum_host);
     delete pb;
     return Q8G_OK;
@@ -379,11 +381,39 @@ int q8g_epilogue_create(const q8g_packed_b* pb, const q8g_requant_params* p,
                         const int32_t* bias_add_host, q8g_epilogue** out) {
     if (!pb || !p || !out) return fail(Q8G_EINVAL, "null argument");
     *out = nullptr;
-    // exactness bound of the int32 adjust (requant.cuh): |adj| <= 255*255*K + |bias|
-    // < 2^31 for K <= 32768 and |bias| < 2^24
-    if (pb->k > 32768)
-        return fail(Q8G_EINVAL, "Requantize: K too large for an exact int32 accumulator");
     const int32_t* colsum = p->col_offsets_host ? p->col_offsets_host : pb->colsum_host;
+    // Exactness of the int32 adjust (requant.cuh): the kernels compute
+    // adj = acc - zp_b*rowsum + c (mod 2^32); it equals the reference's int64
+    // requantize_adjust (quant.hpp:115-125) iff the true value fits int32.
+    // With the weight's own column sums the true value is
+    //   sum_k (A - zp_a)(B - zp_b) + (k_total - K) zp_a zp_b + bias
+    // with A in [0, 255] and |B| <= max|B| (pack time); with caller-supplied
+    // column sums every term is bounded separately.
+    {
+        const int64_t K = pb->k, za = p->zp_a;
+        const int64_t amax = std::max<int64_t>(za < 0 ? -za : za, 255 - za < 0 ? za - 255 : 255 - za);
+        for (int j = 0; j < pb->n; ++j) {
+            const int64_t zb = p->zp_b_per_channel_host ? p->zp_b_per_channel_host[j] : p->zp_b;
+            const int64_t azb = zb < 0 ? -zb : zb;
+            int64_t bias = (p->bias_host ? p->bias_host[j] : 0) + (bias_add_host ? bias_add_host[j] : 0);
+            bias = bias < 0 ? -bias : bias;
+            const int64_t dk = (int64_t)p->k_total - K;
+            int64_t bound;
+            if (!p->col_offsets_host) {
+                bound = K * amax * ((int64_t)pb->max_abs + azb) + (dk < 0 ? -dk : dk) * (za < 0 ? -za : za) * azb + bias;
+            } else {
+                const int64_t cs = colsum[j] < 0 ? -(int64_t)colsum[j] : (int64_t)colsum[j];
+                const int64_t kt = p->k_total < 0 ? -(int64_t)p->k_total : (int64_t)p->k_total;
+                bound = K * 255 * (int64_t)pb->max_abs + azb * 255 * K + (za < 0 ? -za : za) * cs +
+                        kt * (za < 0 ? -za : za) * azb + bias;
+            }
+            if (bound >= (int64_t(1) << 31))
+                return fail(Q8G_EINVAL, "Requantize: the zero-point-adjusted accumulator of column " +
+                                            std::to_string(j) + " can reach " + std::to_string(bound) +
+                                            " >= 2^31 (K, |A - zp_a|, |B - zp_b| or |bias| too large for the "
+                                            "exact int32 epilogue)");
+        }
+    }
     std::vector<EpiRecord> rec;
     bool need_rowsum = false;
     int rc = build_records(pb->n, pb->np, p->k_total, p, colsum, bias_add_host, rec, need_rowsum);
@@ -959,6 +989,15 @@ static int conv_common(const uint8_t* x, int nb, int h, int w, int c, int32_t zp
               : (void*)((uint8_t*)y + (size_t)img_begin * img_px * pw->n);
     cudaError_t e = launch_conv3x3(a, s);
     if (e != cudaSuccess) return cuda_fail(e, "conv3x3 launch");
+    return Q8G_OK;
+}
+
+int q8g_conv3x3_prepare(const q8g_packed_b* pw, int c, void* stream) {
+    if (!pw || c < 1) return fail(Q8G_EINVAL, "conv3x3: bad arguments");
+    if (pw->k != 9 * c) return fail(Q8G_EINVAL, "conv3x3: packed weight K must equal 9*C");
+    DeviceGuard dg(pw->device);
+    const cudaError_t e = conv_tc_prepare(pw, c, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "conv3x3 operand image");
     return Q8G_OK;
 }
 

@@ -25,7 +25,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 
 #include "ptx.cuh"
@@ -533,7 +535,7 @@ CvParams make_params(const ConvArgs& a) {
     p.halo_bytes = (ROWS + 2) * p.wp * p.c;
     p.pb = a.pw->data;
     p.np = a.pw->np;
-    p.img = a.pw->conv_img;
+    p.img = nullptr;
     p.img_bytes = 9 * (p.planes / 2) * 2 * p.nq * 16 + 9 * p.oc_pad * 4;
     p.rec = a.raw ? nullptr : a.ep->rec;
     p.zp_a = a.zp_a;
@@ -562,6 +564,39 @@ bool conv_tc_supported(const ConvArgs& a) {
     return cv_layout(p).total <= 232448;
 }
 
+cudaError_t conv_tc_prepare(const q8g_packed_b* pwc, int c, cudaStream_t s) {
+    if (c != 32 && c != 64 && c != 128) return cudaSuccess;  // not an implicit-GEMM shape: no image
+    static std::mutex mu;
+    const int slot = c == 32 ? 0 : c == 64 ? 1 : 2;
+    auto* pw = const_cast<q8g_packed_b*>(pwc);  // the image is a cache of derived data, not the weight
+    std::lock_guard<std::mutex> lock(mu);
+    if (__atomic_load_n(&pw->conv_img_ready[slot], __ATOMIC_ACQUIRE)) return cudaSuccess;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;  // prepare before capturing
+    ConvArgs a{};
+    a.nb = 1;
+    a.h = 8;
+    a.w = 8;
+    a.c = c;
+    a.pw = pw;
+    a.raw = true;
+    const CvParams p = make_params(a);
+    uint8_t* img = nullptr;
+    cudaError_t e = cudaMalloc(&img, (size_t)p.img_bytes);
+    if (e != cudaSuccess) return e;
+    conv_prep_kernel<<<64, 256, 0, s>>>(p, img);
+    count_launch(kFamPack);
+    if ((e = cudaGetLastError()) == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFree(img);
+        return e;
+    }
+    pw->conv_img[slot] = img;
+    __atomic_store_n(&pw->conv_img_ready[slot], 1, __ATOMIC_RELEASE);
+    return cudaSuccess;
+}
+
 cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     auto enc = tmap_encoder();
     CvParams p = make_params(a);
@@ -579,27 +614,15 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     const CvLayout L = cv_layout(p);
     int dev = 0;
     cudaGetDevice(&dev);
-    // per-weight operand image, built once per (weight, C) on first use (the
-    // first conv call on a weight must not be inside a stream capture)
-    auto* pw = const_cast<q8g_packed_b*>(a.pw);
-    p.img_prefetch = 1;
-    if (pw->conv_img_c != a.c) {
-        p.img_prefetch = 0;
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(s, &cs);
-        if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
-        if (pw->conv_img) cudaFree(pw->conv_img);
-        pw->conv_img = nullptr;
-        pw->conv_img_c = 0;
-        cudaError_t e = cudaMalloc(&pw->conv_img, (size_t)p.img_bytes);
+    // per-weight operand image: built once per (weight, C), synchronously
+    // and under a lock, then immutable (conv_tc_prepare)
+    const int slot = a.c == 32 ? 0 : a.c == 64 ? 1 : 2;
+    if (!__atomic_load_n(&a.pw->conv_img_ready[slot], __ATOMIC_ACQUIRE)) {
+        const cudaError_t e = conv_tc_prepare(a.pw, a.c, s);
         if (e != cudaSuccess) return e;
-        conv_prep_kernel<<<64, 256, 0, s>>>(p, pw->conv_img);
-        count_launch(kFamPack);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        pw->conv_img_c = a.c;
-        pw->conv_img_bytes = (size_t)p.img_bytes;
     }
-    p.img = pw->conv_img;
+    p.img = a.pw->conv_img[slot];
+    p.img_prefetch = 1;
     int grid = sm_count(dev);
     if (grid > p.units) grid = p.units;
     const int mode = a.raw ? 0 : (a.ep->rounding == Q8G_ROUND_F32_RNE ? 1 : 2);

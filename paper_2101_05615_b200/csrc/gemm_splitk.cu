@@ -493,6 +493,10 @@ uint8_t* splitk_workspace(int dev, cudaStream_t s, size_t bytes) {
     static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, std::pair<uint8_t*, size_t>> ws;
     std::lock_guard<std::mutex> lock(mu);
+    // bounded: at most 64 (device, stream) workspaces per process (an app
+    // that creates streams per request would otherwise grow without bound);
+    // further streams get none and take the workspace-free kernel
+    if (ws.size() >= 64 && ws.find({dev, s}) == ws.end()) return nullptr;
     auto& slot = ws[{dev, s}];
     if (slot.second >= bytes) return slot.first;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

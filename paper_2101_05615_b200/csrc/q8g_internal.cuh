@@ -60,12 +60,16 @@ void count_launch(int family);
         if (_e != cudaSuccess) return ::q8g::cuda_fail(_e, #expr); \
     } while (0)
 
-// RAII device guard
+// RAII device guard.  cudaSetDevice is called even when `dev` is already
+// the current device: it makes the device's primary context current in a
+// thread that has not used the runtime yet (a fresh caller thread), which the
+// driver-level tensor-map encoder needs -- without it
+// cuTensorMapEncodeTiled fails with CUDA_ERROR_INVALID_VALUE there.
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
         cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
+        cudaSetDevice(dev);
     }
     ~DeviceGuard() {
         int cur = -1;
@@ -95,11 +99,15 @@ struct q8g_packed_b {
     int8_t* data = nullptr;       // device, kp*np bytes
     int32_t* colsum_dev = nullptr; // device, np entries (zero beyond n)
     int32_t* colsum_host = nullptr;
-    // conv3x3 tensor-core operand image (conv_tc.cu), built once per C:
-    // the smem B layout followed by the per-tap weight sums
-    uint8_t* conv_img = nullptr;
-    int conv_img_c = 0;
-    size_t conv_img_bytes = 0;
+    // conv3x3 tensor-core operand images (conv_tc.cu), one per input-channel
+    // count C in {32, 64, 128}: the smem B layout followed by the per-tap
+    // weight sums.  Built once, synchronously, under a lock
+    // (q8g_conv3x3_prepare or the first conv call); conv_img_ready[i] is
+    // published (release) only when the image is complete, and an image is
+    // never rebuilt or freed before q8g_free_packed_b -- the weight stays
+    // immutable and shareable across streams / threads (pack.hpp:59-62).
+    uint8_t* conv_img[3] = {nullptr, nullptr, nullptr};
+    int conv_img_ready[3] = {0, 0, 0};
 };
 
 struct q8g_epilogue {
@@ -234,6 +242,9 @@ cudaError_t launch_conv3x3_im2col(const ConvArgs& a, cudaStream_t s);
 int default_tile_kind(int rows, int n, int k, bool aligned);
 bool conv_tc_supported(const ConvArgs& a);
 cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s);
+// build the conv operand image of `pw` for C input channels (no-op when the
+// implicit-GEMM kernel does not serve that C or the image exists)
+cudaError_t conv_tc_prepare(const q8g_packed_b* pw, int c, cudaStream_t s);
 
 cudaError_t launch_dwconv3x3(const uint8_t* x, int nb, int h, int w, int c,
                              const q8g_dw_filter* f, uint8_t* y, cudaStream_t s);

@@ -6,8 +6,10 @@
 //   adj = acc - zp_b[j]*rowsum[i] + c[j]
 //       c[j] = bias[j] - zp_a*colsum[j] + K*zp_a*zp_b[j]
 // All int32 arithmetic wraps mod 2^32.  The reference computes `adj` in
-// int64; whenever the true |adj| < 2^31 (guaranteed by the host-side K
-// bound: |adj| <= 255*255*K + |bias|) the wrapped int32 value equals it.
+// int64; whenever the true |adj| < 2^31 the wrapped int32 value equals it,
+// and q8g_epilogue_create rejects parameters for which some column's bound
+// K*max|A - zp_a|*(max|B| + |zp_b|) + |(k_total - K) zp_a zp_b| + |bias|
+// reaches 2^31 (abi.cu).
 #pragma once
 
 #include <stdint.h>

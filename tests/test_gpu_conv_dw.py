@@ -92,6 +92,56 @@ def test_conv3x3_c3_full_vs_oracle(cuda, orc):
     assert torch.equal(y, y2)
 
 
+def test_conv3x3_host_views_chunked_equal_device(cuda, orc):
+    """q8g_conv3x3_u8s8_nhwc_host (the reference convention: host views),
+    chunked with its copies overlapped, equals the oracle at the full C3 size,
+    image sub-ranges included."""
+    cc = configs.conv_case(orc)
+    pw = q8.prepack_conv3x3_weights(cc.w)
+    _, exp = conv_oracle(orc, cc)
+    y = np.zeros((32, 56, 56, 64), dtype=np.uint8)
+    q8.execute_conv3x3(np.ascontiguousarray(cc.x), pw, y, conv_pipeline(cc, 64))
+    assert (y.reshape(-1, 64) == exp).all()
+    y2 = np.full_like(y, 7)
+    q8.execute_conv3x3(np.ascontiguousarray(cc.x), pw, y2, conv_pipeline(cc, 64), image_begin=5, image_end=19)
+    assert (y2[5:19] == y[5:19]).all() and (y2[:5] == 7).all() and (y2[19:] == 7).all()
+
+
+def test_conv3x3_concurrent_first_use_on_two_streams(cuda, orc):
+    """A conv weight packed through the plain GEMM packer (no eager operand
+    image) is used for the first time by two threads on two streams at once:
+    the image is built once under a lock and both outputs are exact
+    (pack.hpp:59-62: a packed weight is shareable across concurrent calls)."""
+    import threading
+    cc = configs.conv_case(orc, 4, 14, 14, 64, 64, seed=21)
+    pw = q8.prepack_weights(cc.w.reshape(9 * 64, 64))  # no q8g_conv3x3_prepare
+    _, exp = conv_oracle(orc, cc)
+    pipe = conv_pipeline(cc, 64)
+    pipe.epilogue(pw)
+    xd = dev(cc.x)
+    ys = [torch.zeros((4, 14, 14, 64), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    errs = []
+    barrier = threading.Barrier(2)
+
+    def work(i):
+        try:
+            barrier.wait()
+            q8.execute_conv3x3(xd, pw, ys[i], pipe, stream=streams[i])
+            streams[i].synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for y in ys:
+        assert (y.cpu().numpy().reshape(-1, 64) == exp).all()
+
+
 def dw_filter(dc: configs.DwCase):
     rp = q8.RequantParams(multiplier=1.0, zp_a=dc.zp_a, zp_c=dc.zp_c, k_total=9, bias=dc.bias,
                           zp_b_per_channel=dc.zp_w, multiplier_f32_per_channel=dc.mult_f32,
@@ -215,6 +265,10 @@ def test_dwconv_c4_full_vs_oracle(cuda, orc):
         q8.execute_dwconv3x3(xd, f, y2, image_begin=i0, image_end=i1)
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
+    # host views (q8g_dwconv3x3_u8s8_nhwc_host: chunked, copies overlapped)
+    yh = np.zeros(dc.x.shape, dtype=np.uint8)
+    q8.execute_dwconv3x3(np.ascontiguousarray(dc.x), f, yh)
+    assert (yh == exp).all()
 
 
 # im2col + tensor-core GEMM: the channel counts real networks use beyond the

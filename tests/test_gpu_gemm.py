@@ -390,6 +390,50 @@ def test_wide_pair_kernel_ragged_shapes(cuda, orc, m, n, k, ldc_pad, mode):
     assert q8.launch_stats()["gemm_tc_large_m"] == before + 1
 
 
+def test_host_view_large_stripe_chunked_pipeline(cuda, orc):
+    """Host-view GEMM of >= 4096 rows (chunked, H2D / GEMM / D2H overlapped on
+    three streams): raw and requantized outputs equal the oracle, a worker
+    stripe included, and a wide host ldc window is left untouched outside."""
+    m, n, k = 5000, 1000, 512
+    c = configs.gemm_case(orc, "C1", m, n, k, seed=77)
+    pw = q8.prepack_weights(c.b)
+    acc = orc.naive_gemm_i32(c.a, c.b)
+    raw = np.zeros((m, n), np.int32)
+    q8.execute_gemm(c.a, pw, raw, q8.OutputPipeline([q8.WriteRawI32()]))
+    assert (raw == acc).all()
+    exp = oracle_requant(orc, c, acc, 1)
+    big = np.full((m, n + 40), 0x5A, np.uint8)
+    view = big[:, 16:16 + n]
+    q8.execute_gemm(c.a, pw, view, requant_pipeline(c, k, q8.ROUND_F32_RNE))
+    assert (view == exp).all() and (big[:, :16] == 0x5A).all() and (big[:, 16 + n:] == 0x5A).all()
+    part = np.zeros((m, n), np.uint8)
+    q8.execute_gemm(c.a, pw, part, requant_pipeline(c, k, q8.ROUND_F32_RNE), thread_id=1, num_threads=2)
+    r0, r1 = q8.api.stripe_rows(m, 1, 2)
+    assert (part[r0:r1] == exp[r0:r1]).all() and (part[:r0] == 0).all()
+
+
+def test_requant_adjust_bound_rejects_inexact_parameters(cuda, orc):
+    """q8g_epilogue_create refuses parameters whose zero-point-adjusted
+    accumulator could leave int32 (the reference computes it in int64,
+    quant.hpp:115-125): a far-off zp_a, a bias near 2^31; borderline
+    legitimate parameters are accepted."""
+    k, n = 4096, 64
+    r = orc.rng(5)
+    pw = q8.prepack_weights(r.i8_matrix(k, n))
+    def ep(**kw):
+        base = dict(zp_a=128, zp_c=5, k_total=k, zp_b=3, multiplier=1e-4, rounding=q8.ROUND_F32_RNE)
+        base.update(kw)
+        return q8.OutputPipeline([q8.Requantize(q8.RequantParams(**base))]).epilogue(pw)
+    ep()
+    ep(bias=np.full(n, 2 ** 29, np.int32))
+    with pytest.raises(q8.InvalidArgument, match="2\\^31"):
+        ep(zp_a=100000)
+    with pytest.raises(q8.InvalidArgument, match="2\\^31"):
+        ep(bias=np.full(n, 2 ** 31 - 1000, np.int32))
+    with pytest.raises(q8.InvalidArgument, match="2\\^31"):
+        ep(zp_b=2 ** 20)
+
+
 def _c2_reference_accumulators(orc, a, b):
     """All 67 M int32 accumulators of C2 on the host: the unmodified reference
     execute_gemm[WriteRawI32] (oracle/_ref) on every host core -- pinned to
