@@ -262,15 +262,18 @@ def timed_graph(run_step, steps, stream, dev, world, sampler_index):
 
 # ---------------------------------------------------------------- reference arm
 
-def cpu_reference_gemm(cfg, threads, budget_s=15.0, max_steps=20, rows=None):
+def cpu_reference_gemm(cfg, threads, budget_s=15.0, max_steps=20, rows=None, build=None):
     """The reference's CPU path on this host on a bounded row sample: unmodified
     q8gemm execute_gemm[WriteRawI32] (oracle/_ref) with `threads` caller-owned
     workers + the restated per-channel fp32 requant (the reference is
-    per-tensor only).  TOPS of the sample."""
-    from oracle.py import Oracle, RefLib  # CPU baseline leg only
+    per-tensor only).  TOPS of the sample.  build: None = the fastest build
+    this host runs (-march=x86-64-v4 on AVX-512 hosts, BASELINE.md §3's
+    -march=native), "release" = the reference's CMake Release flags."""
+    from oracle.py import REF_RELEASE_SO, Oracle, RefLib, best_ref_so  # CPU baseline leg only
     m_all, n, k, alpha_c, _ = GEMM_CONFIGS[cfg]
     m = rows or min(m_all, 1024)
-    orc, ref = Oracle(), RefLib()
+    so = REF_RELEASE_SO if build == "release" else best_ref_so()
+    orc, ref = Oracle(), RefLib(so)
     r = orc.rng(42)
     a = r.u8_matrix(m, k)
     b = r.i8_matrix(k, n)
@@ -298,7 +301,7 @@ def cpu_reference_gemm(cfg, threads, budget_s=15.0, max_steps=20, rows=None):
     return {"value": ops / sec / 1e12, "unit": "TOPS", "cores": threads, "kind": "reference",
             "sample": f"{m} of {cfg}'s {m_all} rows ({m}x{n}x{k}): reference execute_gemm[WriteRawI32] + restated "
                       f"per-channel F32_RNE requant, median of {len(times)}, {threads} std::threads "
-                      f"({busy} row stripes busy)",
+                      f"({busy} row stripes busy); build {so.name}",
             "ms_per_sample": sec * 1e3}
 
 
@@ -318,14 +321,14 @@ def cpu_reference_conv(cfg, threads, budget_s=15.0, images=0):
     """C3: restated im2col + the reference execute_gemm (oracle/_ref) + restated
     per-channel requant; C4: the restated depthwise loop (no reference path),
     on a bounded sample of images of the workload."""
-    from oracle.py import Oracle, RefLib  # CPU baseline leg only
+    from oracle.py import Oracle, RefLib, best_ref_so  # CPU baseline leg only
     _, h, w, c, oc, _, _ = CONV_CONFIGS[cfg]
     orc = Oracle()
     wt, bias, zp_b, mult = conv_inputs(cfg)
     nimg = images or (2 if oc else 1)
     x = np.random.default_rng(5).integers(0, 256, (nimg, h, w, c)).astype(np.uint8)
     if oc:
-        ref = RefLib()
+        ref = RefLib(best_ref_so())
         wk = wt.reshape(9 * c, oc)
         pk = ref.prepack(wk, ref.select_blocking(nimg * h * w, oc, 9 * c))
         colsum = pk.col_offsets()
@@ -671,6 +674,9 @@ def run_ours(args):
                 cb = (cpu_reference_gemm(cfg, os.cpu_count() or 1) if cfg in GEMM_CONFIGS
                       else cpu_reference_conv(cfg, os.cpu_count() or 1))
                 line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+                if cfg in GEMM_CONFIGS:  # the reference's own CMake Release flags, for comparison
+                    rel = cpu_reference_gemm(cfg, os.cpu_count() or 1, budget_s=5.0, max_steps=5, build="release")
+                    line["cpu_baseline"]["release_flags_value"] = rel["value"]
             except Exception as e:  # noqa: BLE001 - the baseline is reported, never the target
                 line["cpu_baseline"] = {"value": None, "unit": "TOPS", "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}

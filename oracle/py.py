@@ -19,6 +19,21 @@ HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libq8ref.so"
 REF_RELEASE_SO = HERE / "_ref" / "libq8ref_release.so"
+REF_V4_SO = HERE / "_ref" / "libq8ref_v4.so"
+
+
+def host_has_avx512() -> bool:
+    try:
+        flags = Path("/proc/cpuinfo").read_text().split("flags")[1].split("\n")[0].split()
+    except (OSError, IndexError):
+        return False
+    return all(f in flags for f in ("avx512f", "avx512bw", "avx512vl", "avx512dq", "avx512cd"))
+
+
+def best_ref_so() -> Path:
+    """The fastest reference build this host can run: -march=x86-64-v4 on
+    AVX-512 hosts (BASELINE.md §3 asks for -march=native), else x86-64-v3."""
+    return REF_V4_SO if REF_V4_SO.exists() and host_has_avx512() else REF_SO
 REF_INCLUDE = Path("/root/reference/proj/include")
 
 _P, _I, _D, _F = C.c_void_p, C.c_int, C.c_double, C.c_float
