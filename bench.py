@@ -235,24 +235,28 @@ def idle_rank_barriers(world):
 
 
 def timed_graph(run_step, steps, stream, dev, world, sampler_index):
-    """Capture `steps` steps in one CUDA graph; time exactly one replay between
-    a barrier + synchronize on both sides (CUDA events on the launching
-    stream) with the clocks sampled during it.  Returns (ms, clocks)."""
+    """Capture `steps` steps in one CUDA graph, with the start / end CUDA
+    events recorded INSIDE the graph as its first and last nodes (on the
+    launching stream), so the timed region is exactly the K steps -- not the
+    host's graph-launch submission, which for a 20-step graph of ~10 us
+    kernels would add ~4 us per step.  One replay, a barrier + synchronize on
+    both sides, clocks sampled during it.  Returns (ms, clocks)."""
     import torch
     import torch.distributed as dist
+    start = torch.cuda.Event(enable_timing=True, external=True)
+    end = torch.cuda.Event(enable_timing=True, external=True)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
+        start.record(stream)
         for i in range(steps):
             run_step(i)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        end.record(stream)
     sampler = ClockSampler(sampler_index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     sampler.start()
-    start.record(stream)
     graph.replay()
-    end.record(stream)
     torch.cuda.synchronize(dev)
     clocks = sampler.stop()
     if world > 1:

@@ -24,11 +24,32 @@ def main():
                           zp_b_per_channel=rng.integers(-10, 11, oc).astype(np.int32),
                           multiplier_f32_per_channel=np.full(oc, 0.0005, np.float32), rounding=q8.ROUND_F32_RNE)
     pipe = q8.OutputPipeline([q8.ReluQuantized(), q8.Requantize(rp)])
-    x = torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device="cuda")
-    y = torch.empty((nb, h, w, oc), dtype=torch.uint8, device="cuda")
+    # --graph N: the last of N back-to-back launches replayed from a CUDA graph
+    # over 22 rotating buffer sets (> 2x L2, as bench.py) -- the steady state
+    nsets = 22 if "--graph" in sys.argv else 1
+    xs = [torch.randint(0, 256, (nb, h, w, c), dtype=torch.uint8, device="cuda") for _ in range(nsets)]
+    ys = [torch.empty((nb, h, w, oc), dtype=torch.uint8, device="cuda") for _ in range(nsets)]
+    x, y = xs[0], ys[0]
     for _ in range(3):
         q8.execute_conv3x3(x, pw, y, pipe)
     torch.cuda.synchronize()
+    if "--graph" in sys.argv:
+        steps = int(sys.argv[sys.argv.index("--graph") + 1])
+        s = torch.cuda.Stream()
+        torch.cuda.set_stream(s)
+        for i in range(nsets):
+            q8.execute_conv3x3(xs[i], pw, ys[i], pipe)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(steps):
+                q8.execute_conv3x3(xs[i % nsets], pw, ys[i % nsets], pipe)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+        torch.cuda.synchronize()
+        print(f"graph of {steps}: {e0.elapsed_time(e1) * 1e3 / steps:.2f} us per launch")
     buf = (C.c_uint64 * (8 * 1024 + 2048))()
     _lib.load().q8g_debug_tc_trace(buf, 2048)
     a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
@@ -47,6 +68,8 @@ def main():
     for i in range(n):
         print(f"{i:4d} " + " ".join(f"{(units[j, i] - t0) / 1e3:9.2f}" for j in range(5)) +
               f" {(tl[i] - t0) / 1e3:9.2f} {(w5[i] - t0) / 1e3:9.2f} {(w6[i] - t0) / 1e3:9.2f}")
+
+
 
 
 if __name__ == "__main__":
