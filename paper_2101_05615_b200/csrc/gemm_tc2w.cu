@@ -85,7 +85,7 @@ struct Cfg {
     static constexpr int OUT_WARP = 32 * 64;
     static constexpr int BAR_OFF = OUT_OFF + 8 * OUT_WARP;
     // full[S], empty[S], rsdone[S], tfull[2], tempty[2], rfull[2], rempty[2]
-    static constexpr int NUM_BARS = 3 * STAGES + 8;
+    static constexpr int NUM_BARS = 4 * STAGES + 8;  // + aread[S] (row-sum warps: the stage's A was read)
     static constexpr int RS_OFF = BAR_OFF + NUM_BARS * 8;
     static constexpr int REC_OFF = RS_OFF + 2 * BM * 4;  // the tile's column records, SoA: c, zp_b, mult lo, hi
     static constexpr int TMEMPTR_OFF = REC_OFF + 4 * PN * 4;
@@ -247,6 +247,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto rsdone_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
+    // committed (multicast) after a stage's half-0 MMAs: its A has landed and
+    // stays until the stage's empty barrier -- the row-sum warps read from
+    // here, ahead of the half-1 MMAs (the tile-end skew puts two K blocks of
+    // half-1 MMAs after the last half-0 MMA)
+    auto aread_bar = [&](int s) { return bar0 + 8u * (3 * STAGES + 8 + s); };
     auto tfull_bar = [&](int h) { return bar0 + 8u * (3 * STAGES + h); };
     auto tempty_bar = [&](int h) { return bar0 + 8u * (3 * STAGES + 2 + h); };
     auto rfull_bar = [&](int b) { return bar0 + 8u * (3 * STAGES + 4 + b); };
@@ -262,6 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(full_bar(s), 1);    // leader: its own producer's expect_tx arrive
             ptx::mbar_init(empty_bar(s), 1);   // the leader's multicast commit
             ptx::mbar_init(rsdone_bar(s), 2);  // this CTA's two row-sum warps
+            ptx::mbar_init(aread_bar(s), 1);
         }
         for (int h = 0; h < 2; ++h) {
             ptx::mbar_init(tfull_bar(h), 1);
@@ -289,21 +295,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t full_leader0 = ptx::mapa_shared(full_bar(0), 0);
         int stage = 0;
         uint32_t phase = 0;
-        uint32_t rs_pending = 0, rs_par = 0;  // per stage: last use was a row-sum use / rsdone parity
-        int prev_m = -1;
         for (int t = tr.first; t < tr.last; t += tr.step) {
             const int mt = t / nt, ntile = t % nt;
-            const bool rs_tile = RS && mt != prev_m;
-            prev_m = mt;
             const int m0 = mt * 2 * BM + (int)rank * BM;
             const int brow = ntile * PN + (int)rank * HN;  // this CTA's columns of sub-tile 0
             for (int kb = 0; kb < p.nkb; ++kb) {
                 ptx::mbar_wait(empty_bar(stage), phase ^ 1);
-                if (RS && ((rs_pending >> stage) & 1u)) {  // row-sum warps still reading this stage
-                    ptx::mbar_wait(rsdone_bar(stage), (rs_par >> stage) & 1u);
-                    rs_par ^= 1u << stage;
-                }
-                rs_pending = (rs_pending & ~(1u << stage)) | ((rs_tile ? 1u : 0u) << stage);
+                // the row-sum warps arrive once per use of every stage (reading
+                // it on row-sum tiles): they are done with the previous use
+                if (RS) ptx::mbar_wait(rsdone_bar(stage), phase ^ 1);
                 if (ptx::elect_one()) {
                     if (leader) ptx::mbar_arrive_expect_tx(full_bar(stage), 2 * STAGE);
                     const uint32_t fb = full_leader0 + 8u * stage;
@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int ks = 0; ks < kKBlock / 32; ++ks)
                     ptx::mma_i8_pair(tmem_base + (uint32_t)(h * 2 * HN), adesc + 2 * ks, bdesc + 2 * ks, idesc,
                                      (kb | ks) != 0);
+                if (RS && h == 0) ptx::tc_commit_pair_mc(aread_bar(s), 0x3);  // (before the stage's half-1 MMAs)
                 if (kb == nkb - 1) {
                     ptx::tc_commit_pair_mc(tfull_bar(h), 0x3);
                     tw_tile(p, 2 + h, ti);
@@ -410,10 +411,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (rs_tile) ptx::mbar_wait(rempty_bar(b), ((run >> 1) & 1) ^ 1);
             uint32_t s0 = 0, s1 = 0;
             for (int kb = 0; kb < p.nkb; ++kb) {
-                // the MMA has consumed the stage: its data has landed and, on a
-                // row-sum tile, stays until this warp arrives on rsdone (the
-                // producer waits for it before reloading the stage)
-                ptx::mbar_wait_cluster(empty_bar(stage), phase);
+                // the stage's half-0 MMAs are complete: its A has landed and
+                // stays until this warp arrives on rsdone (the producer waits
+                // for that, on every use, before reloading the stage)
+                ptx::mbar_wait_cluster(aread_bar(stage), phase);
                 if (rs_tile) {
                     const uint8_t* sa = smem + stage * STAGE;
 #pragma unroll
@@ -431,9 +432,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                         s1 = ptx::dp4a_uu(w1.z, 0x01010101u, s1);
                         s1 = ptx::dp4a_uu(w1.w, 0x01010101u, s1);
                     }
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(rsdone_bar(stage));
                 }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(rsdone_bar(stage));
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
