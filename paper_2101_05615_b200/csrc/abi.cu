@@ -827,6 +827,19 @@ int run_host_pipeline(int device, cudaStream_t s, const HostPipeSpec& sp, F comp
 }
 }  // namespace
 
+// rows per chunk of the host-view GEMM pipeline (Q8G_HOST_CHUNK overrides, A/B)
+static int host_chunk_rows(int rows) {
+    static const int env = [] {
+        const char* e = getenv("Q8G_HOST_CHUNK");
+        return e ? atoi(e) : 0;
+    }();
+    if (env > 0) return round_up_i(env, 256);
+    // C2 (16384 rows), host wall time per call: 1024-row chunks 2.02 ms,
+    // 2048 1.81, 4096 1.83, 8192 2.13 (the copies alone, both directions
+    // concurrently: 1.38 ms) -- per-chunk overhead vs pipeline fill
+    return round_up_i(std::max(2048, rows / 8), 256);
+}
+
 template <typename OutT>
 static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_packed_b* pb,
                      const q8g_epilogue* ep, OutT* c_host, int ldc, int row_begin, int row_end,
@@ -841,11 +854,11 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
     DeviceGuard dg(pb->device);
     const int lda_d = round_up_i(k, 16), ldc_d = pb->n;
     if (rows >= 4096) {
-        // large stripes: chunks of >= 1024 rows (multiples of the 256-row
+        // large stripes: chunks of >= 2048 rows (multiples of the 256-row
         // pair tile), copies overlapped with the GEMM of the previous chunk
         HostPipeSpec sp{a_host + (size_t)row_begin * lda, (size_t)lda, (size_t)k, (size_t)lda_d,
                         reinterpret_cast<uint8_t*>(c_host + (size_t)row_begin * ldc), sizeof(OutT) * ldc,
-                        sizeof(OutT) * pb->n, sizeof(OutT) * ldc_d, rows, round_up_i(std::max(1024, rows / 16), 256)};
+                        sizeof(OutT) * pb->n, sizeof(OutT) * ldc_d, rows, host_chunk_rows(rows)};
         return run_host_pipeline(pb->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
             return gemm_common(din, u1 - u0, k, lda_d, pb, raw ? nullptr : ep, nullptr, dout, ldc_d, 0, u1 - u0,
                                nullptr, s, raw);
