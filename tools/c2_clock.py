@@ -46,6 +46,8 @@ def main():
         with torch.cuda.graph(g, stream=s):
             for i in range(cnt):
                 q8.execute_gemm(As[i % 2], pw, Cs[i % 2], pipe)
+        g.replay()  # the first replay of a fresh graph also uploads it
+        torch.cuda.synchronize()
         time.sleep(1.0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
