@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <mutex>
 #include <cmath>
@@ -49,6 +50,42 @@ int sm_count(int device) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
     if (device >= 0 && device < 64) cache[device] = v;
     return v;
+}
+
+namespace {
+struct WorkRing {
+    int* base = nullptr;
+    std::atomic<unsigned> next{0};
+};
+WorkRing g_work_ring[64];
+std::mutex g_work_mu;
+}  // namespace
+
+cudaError_t work_slot_prepare(int device) {
+    if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(g_work_mu);
+    if (__atomic_load_n(&g_work_ring[device].base, __ATOMIC_ACQUIRE)) return cudaSuccess;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    int* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(int) * 2 * kWorkSlots);
+    if (e == cudaSuccess && (e = cudaMemset(p, 0, sizeof(int) * 2 * kWorkSlots)) == cudaSuccess)
+        e = cudaDeviceSynchronize();
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        if (p) cudaFree(p);
+        return e;
+    }
+    __atomic_store_n(&g_work_ring[device].base, p, __ATOMIC_RELEASE);
+    return cudaSuccess;
+}
+
+int* work_slot(int device) {
+    if (device < 0 || device >= 64) return nullptr;
+    int* b = __atomic_load_n(&g_work_ring[device].base, __ATOMIC_ACQUIRE);
+    if (!b) return nullptr;
+    return b + 2 * (g_work_ring[device].next.fetch_add(1, std::memory_order_relaxed) % kWorkSlots);
 }
 
 bool pdl_enabled() {

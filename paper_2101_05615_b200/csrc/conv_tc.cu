@@ -45,6 +45,15 @@ constexpr int ROWS = 2;      // output rows per unit (ROWS * (W+2) <= 128 -> one
 constexpr int MAX_BUF = 8;   // halo buffers in flight: p.nbuf <= MAX_BUF, as many as fit in smem
 constexpr int EPI_WARPS = 8;  // two warpgroups; warpgroup g takes every other unit
 constexpr int MAX_ACC = 4;    // TMEM accumulators (nacc = 4 when nq <= 128, else 2)
+// The producer claims units (dynamically when p.work is set: CTAs that enter
+// late -- their SM was still running the previous launch -- take fewer) and
+// publishes local unit i's id in ring slot i % UNIT_RING as (i << 32 | id + 1),
+// id + 1 = 0 meaning "no more units"; MMA and epilogue warps spin on the tag.
+// The producer runs at most MAX_BUF + MAX_ACC units ahead of the slowest
+// reader, so a slot is never overwritten before it is read.
+constexpr int UNIT_RING = 16;
+static_assert(UNIT_RING >= MAX_BUF + MAX_ACC + 2, "unit ring too small");
+constexpr int DYN_LEAD = 4;  // dynamic claims: units in flight per CTA (see the producer)
 
 struct CvParams {
     int nb, h, w, c, oc;
@@ -67,6 +76,8 @@ struct CvParams {
     int img_prefetch; // operand image built by an earlier call: load it before griddepcontrol.wait
     void* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): CTA 0 per-unit stamps, else null
+    int* work;          // {claim, done} counters of this launch's work slot, or null: static schedule
+    int nstatic;        // static units per CTA before dynamic claiming
 };
 
 // CTA 0, local unit i < 64: [8192 + 64*which + i]; which: 0 halo issued,
@@ -81,7 +92,7 @@ __device__ __forceinline__ void cv_stamp(const CvParams& p, int which, int i) {
     }
 }
 
-// CTA 0 prologue stamps [9344 + k]: 0 barriers/image issued, 1 guards zeroed, 2 TMEM allocated
+// CTA 0 prologue stamps [9344 + k]: 0 barriers/image issued (after 1), 1 guards zeroed, 2 TMEM allocated
 __device__ __forceinline__ void cv_pstamp(const CvParams& p, int k) {
     if (p.trace && blockIdx.x == 0) {
         unsigned long long t;
@@ -90,10 +101,25 @@ __device__ __forceinline__ void cv_pstamp(const CvParams& p, int k) {
     }
 }
 
+// unit ring (see UNIT_RING): tag = local unit index, value = id + 1 (0: none)
+__device__ __forceinline__ void ring_put(uint32_t addr, int i, int id_plus1) {
+    const unsigned long long v = ((unsigned long long)(uint32_t)i << 32) | (uint32_t)id_plus1;
+    asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ring_get(uint32_t addr, int i) {
+    unsigned long long v;
+    asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    while ((uint32_t)(v >> 32) != (uint32_t)i) {
+        __nanosleep(32);
+        asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    }
+    return (int)(uint32_t)v;
+}
+
 __host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
 
 struct CvLayout {
-    int halo_off, halo_stride, b_off, wsum_off, corr_off, rec_off, soa_off, bar_off, tmemptr_off, total;
+    int halo_off, halo_stride, b_off, wsum_off, corr_off, rec_off, soa_off, bar_off, tmemptr_off, ring_off, total;
 };
 __host__ __device__ inline CvLayout cv_layout(const CvParams& p) {
     CvLayout L;
@@ -108,7 +134,8 @@ __host__ __device__ inline CvLayout cv_layout(const CvParams& p) {
     L.soa_off = L.rec_off + p.oc_pad * 16;       // [oc_pad] epilogue records (zp_b, mult)
     L.bar_off = L.soa_off + p.oc_pad * 8;        // SoA: zp_b[oc_pad], mult_f32[oc_pad]
     L.tmemptr_off = L.bar_off + (2 * MAX_BUF + 2 * MAX_ACC + 1) * 8;  // + the operand-image barrier
-    L.total = L.tmemptr_off + 16 + 1024;
+    L.ring_off = L.tmemptr_off + 16;                                   // unit ring: UNIT_RING x u64
+    L.total = L.ring_off + 8 * UNIT_RING + 1024;
     return L;
 }
 
@@ -241,10 +268,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         p.trace[8704 + blockIdx.x] = t;
     }
 
-    // ---- barriers first, then everything overlaps: the producer streams
-    // halos while the operand image (B = [weights | ones] + tap weight sums,
-    // built once per weight by conv_prep_kernel) lands and the epilogue
-    // warps build their correction tables
+    // ---- guard bands, barriers, then everything overlaps: the producer
+    // streams halos while the operand image (B = [weights | ones] + tap weight
+    // sums, built once per weight by conv_prep_kernel) lands and the epilogue
+    // warps build their correction tables.  The image load is issued after
+    // the issuing thread's proxy fence: a fence issued behind it waits for
+    // its 46 KB to land (~0.9 us of prologue, tools/conv_trace.py)
+    // halo guard bands (windows start one position early / run past the end)
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) reinterpret_cast<uint4*>(smem + L.halo_off - 1024)[i] = make_uint4(0, 0, 0, 0);
+    for (int b = 0; b < p.nbuf; ++b) {
+        uint4* g = reinterpret_cast<uint4*>(smem + L.halo_off + b * L.halo_stride + p.halo_bytes);
+        for (int i = threadIdx.x; i < (L.halo_stride - p.halo_bytes) / 16; i += blockDim.x) g[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (threadIdx.x == 0) cv_pstamp(p, 3);
+    if (threadIdx.x < UNIT_RING)  // tags no unit index matches
+        reinterpret_cast<unsigned long long*>(smem + L.ring_off)[threadIdx.x] = ~0ull;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) cv_pstamp(p, 1);
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmap_x);
         ptx::mbar_init(img_bar, 1);
@@ -265,14 +305,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         }
         cv_pstamp(p, 0);
     }
-    // halo guard bands (windows start one position early / run past the end)
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) reinterpret_cast<uint4*>(smem + L.halo_off - 1024)[i] = make_uint4(0, 0, 0, 0);
-    for (int b = 0; b < p.nbuf; ++b) {
-        uint4* g = reinterpret_cast<uint4*>(smem + L.halo_off + b * L.halo_stride + p.halo_bytes);
-        for (int i = threadIdx.x; i < (L.halo_stride - p.halo_bytes) / 16; i += blockDim.x) g[i] = make_uint4(0, 0, 0, 0);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (threadIdx.x == 0) cv_pstamp(p, 1);
     if (warp == W_ALLOC) {
         ptx::tmem_alloc<512>(ptx::smem_u32(tmem_ptr));
         if (lane == 0) cv_pstamp(p, 2);
@@ -291,30 +323,64 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
 
     if (warp == W_PROD) {
         // ------------------------------------------------ halo producer
+        // Schedule: the first p.nstatic units of every CTA are static
+        // (blockIdx.x + i * gridDim.x, all issued at once); the rest are
+        // claimed one at a time from the launch's work slot (counter value c
+        // -> unit nstatic * gridDim.x + c), each only once the MMA of the unit
+        // DYN_LEAD places earlier has completed.  A CTA then holds at most
+        // DYN_LEAD units when the counter runs out, so CTAs that entered late
+        // (their SM was still running the previous grid) take fewer units and
+        // the grid's CTAs finish together.  The lead covers the claim's
+        // atomic round trip (~0.8 us under contention) plus the halo load.
+        const int lead = p.nbuf < DYN_LEAD ? p.nbuf : DYN_LEAD;  // <= nbuf: no phase aliasing
         ptx::griddep_wait();
         if (!p.img_prefetch && ptx::elect_one()) {  // image built by this call's conv_prep_kernel
             ptx::mbar_arrive_expect_tx(img_bar, (uint32_t)p.img_bytes);
             ptx::bulk_load(base + L.b_off, p.img, (uint32_t)p.img_bytes, img_bar);
         }
         __syncwarp();
-        int b = 0;
-        uint32_t ph = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const uint32_t ring = base + L.ring_off;
+        int i = 0;
+        for (;; ++i) {
+            int u = (int)blockIdx.x + i * (int)gridDim.x;
+            if (p.work && i >= p.nstatic) {
+                if (i >= lead) {  // the MMA of unit i - lead has completed
+                    const int j = i - lead;
+                    ptx::mbar_wait(empty_bar(j % p.nbuf), (uint32_t)(j / p.nbuf) & 1u);
+                }
+                if (lane == 0) u = p.nstatic * (int)gridDim.x + atomicAdd(p.work, 1);
+                u = __shfl_sync(0xffffffffu, u, 0);
+            }
+            if (u >= p.units) break;
+            const int b = i % p.nbuf;
+            ptx::mbar_wait(empty_bar(b), ((uint32_t)(i / p.nbuf) & 1u) ^ 1u);
             const int n = u / p.rblocks, rb = u % p.rblocks;
-            ptx::mbar_wait(empty_bar(b), ph ^ 1);
             if (ptx::elect_one()) {
+                ring_put(ring + 8u * (uint32_t)(i % UNIT_RING), i, u + 1);
                 // one 4D TMA: (ROWS+2) rows x (W+2) positions x C bytes, natural
                 // NHWC order, hardware swizzle of span C, out-of-image taps zero
                 ptx::mbar_arrive_expect_tx(full_bar(b), (uint32_t)p.halo_bytes);
                 tma_load_4d(base + L.halo_off + b * L.halo_stride, &tmap_x, 0, -1, rb * ROWS - 1, n, full_bar(b));
-                cv_stamp(p, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
+                cv_stamp(p, 0, i);
             }
             __syncwarp();
-            if (++b == p.nbuf) {
-                b = 0;
-                ph ^= 1;
+        }
+        if (lane == 0) {
+            // "no more units" for both parities (MMA warps / epilogue warpgroups
+            // take alternate units)
+            ring_put(ring + 8u * (uint32_t)(i % UNIT_RING), i, 0);
+            ring_put(ring + 8u * (uint32_t)((i + 1) % UNIT_RING), i + 1, 0);
+            if (p.work) {
+                // every CTA has made its last claim when done reaches the grid
+                // size: the last one zeroes the slot for its next use
+                __threadfence();
+                if (atomicAdd(p.work + 1, 1) == (int)gridDim.x - 1) {
+                    atomicExch(p.work, 0);
+                    atomicExch(p.work + 1, 0);
+                }
             }
         }
+        __syncwarp();
     } else if (warp == W_MMA0 || warp == W_MMA1) {
         // ------------------------------------------------ MMA issuer
         // The whole warp runs the loop (warp-uniform control flow) and one
@@ -336,9 +402,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         // them usually has the next unit's MMAs queued
         const int q = warp == W_MMA0 ? 0 : 1;
         ptx::mbar_wait(img_bar, 0);
-        int ui = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
-            if ((ui & 1) != q) continue;
+        const uint32_t ring = base + L.ring_off;
+        for (int ui = q;; ui += 2) {
+            if (ring_get(ring + 8u * (uint32_t)(ui % UNIT_RING), ui) == 0) break;
             const int b = ui % p.nbuf, acc = ui % p.nacc;
             const uint32_t ph = (uint32_t)(ui / p.nbuf) & 1u, aph = (uint32_t)(ui / p.nacc) & 1u;
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
@@ -464,9 +530,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                     }
                 }
         };
-        int i = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++i) {
-            if ((i & 1) != wg) continue;
+        const uint32_t ring = base + L.ring_off;
+        for (int i = wg;; i += 2) {
+            const int u = ring_get(ring + 8u * (uint32_t)(i % UNIT_RING), i) - 1;
+            if (u < 0) break;
             const int acc = i % p.nacc;
             const uint32_t aph = (uint32_t)(i / p.nacc) & 1u;
             const int n = u / p.rblocks, rb = u % p.rblocks;
@@ -574,6 +641,7 @@ cudaError_t conv_tc_prepare(const q8g_packed_b* pwc, int c, cudaStream_t s) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
     if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;  // prepare before capturing
+    if (const cudaError_t e = work_slot_prepare(pw->device); e != cudaSuccess) return e;
     ConvArgs a{};
     a.nb = 1;
     a.h = 8;
@@ -623,8 +691,25 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     }
     p.img = a.pw->conv_img[slot];
     p.img_prefetch = 1;
+    // dynamic unit claiming (Q8G_CONV_DYN=0: the static round-robin schedule)
+    static const bool dyn = [] {
+        const char* e = getenv("Q8G_CONV_DYN");
+        return !(e && e[0] == '0');
+    }();
     int grid = sm_count(dev);
     if (grid > p.units) grid = p.units;
+    // static head: all but the last unit of an even share (C3: 5 static + ~1
+    // claimed; more claimed units measured slower, the claims contend)
+    p.nstatic = std::max(0, p.units / grid - 1);
+    if (const char* e = getenv("Q8G_CONV_NSTATIC")) p.nstatic = std::max(0, std::atoi(e));
+    if (dyn) {
+        p.work = work_slot(dev);
+        if (!p.work) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(s, &cs);
+            if (cs == cudaStreamCaptureStatusNone && work_slot_prepare(dev) == cudaSuccess) p.work = work_slot(dev);
+        }
+    }
     const int mode = a.raw ? 0 : (a.ep->rounding == Q8G_ROUND_F32_RNE ? 1 : 2);
     const int ks = a.c / 32;
     const int threads = 128 + 32 * EPI_WARPS;

@@ -257,6 +257,17 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
                                 uint8_t* y, cudaStream_t s);
 
 int sm_count(int device);
+// Dynamic work claiming for persistent kernels (conv3x3_tc): a per-device
+// ring of kWorkSlots zeroed {claim, done} int pairs.  Each launch takes the
+// next slot; its CTAs claim units with atomicAdd on slot[0] and the last CTA
+// to finish (slot[1] reaching gridDim) zeroes both for the slot's next use
+// kWorkSlots launches later (or the same captured graph node's next replay,
+// which is stream-ordered after this one).  work_slot_prepare allocates the
+// ring (not allowed under stream capture); work_slot returns nullptr when it
+// is not allocated, and the kernel then falls back to its static schedule.
+constexpr int kWorkSlots = 1024;
+cudaError_t work_slot_prepare(int device);
+int* work_slot(int device);
 // programmatic dependent launch for the tensor-core kernels (env Q8G_PDL=0
 // disables): the kernels trigger their dependents at entry and run their
 // global-memory-free prologue before griddepcontrol.wait

@@ -60,8 +60,14 @@ def main():
     print(f"grid span: first entry {(ent.min() - t0) / 1e3:.2f}  last entry {(ent.max() - t0) / 1e3:.2f}  "
           f"first exit {(ext.min() - t0) / 1e3:.2f}  last exit {(ext.max() - t0) / 1e3:.2f} us; "
           f"CTA0 exit {(ext[0] - t0) / 1e3:.2f}")
+    ee, xx = (ent - t0) / 1e3, (ext - t0) / 1e3
+    order = np.argsort(xx)
+    print("exit percentiles (us):", " ".join(f"p{q}={np.percentile(xx, q):.2f}" for q in (0, 10, 50, 90, 100)))
+    print("latest 12 exits (cta: entry -> exit):",
+          "  ".join(f"{i}: {ee[i]:.2f}->{xx[i]:.2f}" for i in order[-12:]))
+    print("corr(entry, exit) =", f"{np.corrcoef(ee, xx)[0, 1]:.2f}")
     print(f"kernel entry at 0; barriers+image issued {(a[9344] - t0) / 1e3:.2f}, guards zeroed {(a[9345] - t0) / 1e3:.2f}, "
-          f"TMEM allocated {(a[9346] - t0) / 1e3:.2f}, prologue done at {(a[8192 + 320] - t0) / 1e3:.2f} us")
+          f"TMEM allocated {(a[9346] - t0) / 1e3:.2f}, guard stores done {(a[9347] - t0) / 1e3:.2f}, prologue done at {(a[8192 + 320] - t0) / 1e3:.2f} us")
     n = int((units[0] > 0).sum())
     tl = a[8192 + 384:8192 + 448]
     w5, w6 = a[9216:9216 + 64], a[9280:9280 + 64]
