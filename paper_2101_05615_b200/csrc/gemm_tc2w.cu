@@ -149,6 +149,17 @@ __device__ __forceinline__ void tw_tile(const Tc2wParams& p, int k, int ti) {
     }
 }
 
+// CTA 0 epilogue warp 4, per tile ti < 16: [9472 + 8 * ti + k], k = 6 + h:
+// half h's row sums in hand, 3h + 0: half h round 0 requantized, 3h + 1: round 1 staging tile free, 3h + 2:
+// round 1 requantized (tools/tc2w_tiles.py)
+__device__ __forceinline__ void tw_epi(const Tc2wParams& p, int k, int ti) {
+    if (p.trace && blockIdx.x == 0 && ti < 16) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[9472 + 8 * ti + k] = t;
+    }
+}
+
 __device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* m, int c0, int c1,
                                                       uint32_t bar_cluster, uint64_t policy) {
     asm volatile(
@@ -178,20 +189,27 @@ __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
 
 // 16 accumulator columns of one row -> 16 u8, F32_RNE fast path (the
 // arithmetic of epilogue.cuh requant4_f32_fast, records from shared memory):
-// adj = v + c - zp_b*rowsum (wrapping int32), x = RN(float(adj) * mult)
+// adj = v + c + zp_b*(-rowsum) (wrapping int32; -rowsum once per row, not a
+// negation per value), x = RN(float(adj) * mult)
 // (paired RN multiplies), floor, magic add, saturating pack
 __device__ __forceinline__ uint4 requant16_fast(const uint32_t* v, const int32_t* rc, const int32_t* rz,
-                                                const float* rm, int32_t rowsum, int32_t zoff, float floor_x) {
+                                                const float* rm, uint32_t nrowsum, int32_t zoff, float floor_x) {
     uint32_t words[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
+#ifdef Q8G_EXP_NOREC
+        const int4 C = make_int4(w, w + 1, w + 2, w + 3);
+        const int4 Z = make_int4(1, 2, 3, 4);
+        const float4 M = make_float4(1e-4f, 2e-4f, 3e-4f, 4e-4f);
+#else
         const int4 C = *reinterpret_cast<const int4*>(rc + 4 * w);
         const int4 Z = *reinterpret_cast<const int4*>(rz + 4 * w);
         const float4 M = *reinterpret_cast<const float4*>(rm + 4 * w);
-        const int32_t a0 = (int32_t)(v[4 * w + 0] + (uint32_t)C.x - (uint32_t)Z.x * (uint32_t)rowsum);
-        const int32_t a1 = (int32_t)(v[4 * w + 1] + (uint32_t)C.y - (uint32_t)Z.y * (uint32_t)rowsum);
-        const int32_t a2 = (int32_t)(v[4 * w + 2] + (uint32_t)C.z - (uint32_t)Z.z * (uint32_t)rowsum);
-        const int32_t a3 = (int32_t)(v[4 * w + 3] + (uint32_t)C.w - (uint32_t)Z.w * (uint32_t)rowsum);
+#endif
+        const int32_t a0 = (int32_t)(v[4 * w + 0] + ((uint32_t)C.x + (uint32_t)Z.x * nrowsum));
+        const int32_t a1 = (int32_t)(v[4 * w + 1] + ((uint32_t)C.y + (uint32_t)Z.y * nrowsum));
+        const int32_t a2 = (int32_t)(v[4 * w + 2] + ((uint32_t)C.z + (uint32_t)Z.z * nrowsum));
+        const int32_t a3 = (int32_t)(v[4 * w + 3] + ((uint32_t)C.w + (uint32_t)Z.w * nrowsum));
         uint64_t x01 = f32x2_mul(pack2(__int2float_rn(a0), __int2float_rn(a1)), pack2(M.x, M.y));
         uint64_t x23 = f32x2_mul(pack2(__int2float_rn(a2), __int2float_rn(a3)), pack2(M.z, M.w));
         // the floor sits between the multiply and the magic add, so the two
@@ -509,6 +527,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(rempty_bar(b));
                 }
+                if (warp == 4 && lane == 0) tw_epi(p, 6 + h, ti);  // row sums in hand
+                const uint32_t nrowsum = 0u - (uint32_t)rowsum;
                 const int lc0 = h * 2 * HN + g * HN;  // tile-local column of v[0]
                 const int col0 = ntile * PN + lc0;
                 if constexpr (MODE == 3) {
@@ -520,11 +540,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int rd = 0; rd < 2; ++rd) {
                         if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
                         __syncwarp();
+                        if (rd == 1 && warp == 4 && lane == 0) tw_epi(p, 3 * h + 1, ti);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const int cc = rd * 4 + c;
                             const uint4 w = requant16_fast(v + cc * 16, rc + lc0 + cc * 16, rz + lc0 + cc * 16,
-                                                           reinterpret_cast<const float*>(rm) + lc0 + cc * 16, rowsum,
+                                                           reinterpret_cast<const float*>(rm) + lc0 + cc * 16, nrowsum,
                                                            zoff, floor_x);
                             const uint32_t dst = stg + (uint32_t)(lane * 64 + ((c ^ ((lane >> 1) & 3)) * 16));
                             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(w.x), "r"(w.y),
@@ -533,6 +554,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         __syncwarp();
+                        if (warp == 4 && lane == 0) tw_epi(p, 3 * h + 2 * rd, ti);
                         if (lane == 0) tma_store_2d(&tmap_c, stg, col0 + rd * 64, mt * 2 * BM + (int)rank * BM + q * 32);
                     }
                 } else if (valid) {

@@ -38,7 +38,9 @@ def main():
     _lib.load().q8g_debug_tc_trace(buf, 2048)
     w = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
     tiles = w[9216:9216 + 128].reshape(16, 8)
-    tiles = tiles[tiles[:, 0] > 0]
+    epi = w[9472:9472 + 128].reshape(16, 8)
+    keep = tiles[:, 0] > 0
+    tiles, epi = tiles[keep], epi[keep]
     t0 = tiles[0, 0]
     clk, ns = w[10201] - w[10200], w[10203] - w[10202]
     print(f"launch: {ns / 1e3:.1f} us at {clk / max(ns, 1) * 1e3:.0f} MHz")
@@ -46,6 +48,10 @@ def main():
     for i, r in enumerate(tiles):
         span = (tiles[i + 1, 0] - r[0]) / 1e3 if i + 1 < len(tiles) else float("nan")
         print(f"{i:4d} " + " ".join(f"{(x - t0) / 1e3:8.2f}" for x in r) + f"   {span:8.2f}")
+    print("epilogue warp 4, per half: row sums in hand / round-0 requant done / round-1 staging free / "
+          "round-1 requant done (us)")
+    for i, e in enumerate(epi):
+        print(f"{i:4d} " + " ".join(f"{(x - t0) / 1e3:8.2f}" for x in (e[6], *e[0:3], e[7], *e[3:6])))
 
 
 if __name__ == "__main__":
