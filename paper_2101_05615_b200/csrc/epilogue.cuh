@@ -36,12 +36,12 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
 // bits(y) - (0x4B400000 - zp_c) = clamp(rint(x) + zp_c, relu ? zp_c : 0, 255)
 // exactly (bits(y) - 0x4B400000 = rint(x) for |x| <= 2^22 and monotone beyond;
 // requires 0 <= zp_c <= 255 and finite multipliers: fast_f32)
-__device__ __forceinline__ uint32_t requant4_f32_fast(const uint32_t* v, const int4* r4, int32_t rowsum,
+__device__ __forceinline__ uint32_t requant4_f32_fast(const uint32_t* v, const int4* r4, uint32_t nrowsum,
                                                       int32_t zoff, float floor_x) {
     int32_t rr[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-        const int32_t adj = (int32_t)(v[b] + (uint32_t)r4[b].x - (uint32_t)r4[b].y * (uint32_t)rowsum);
+        const int32_t adj = (int32_t)(v[b] + ((uint32_t)r4[b].x + (uint32_t)r4[b].y * nrowsum));
         float x = __fmul_rn(__int2float_rn(adj), __int_as_float(r4[b].z));
         x = fmaxf(x, floor_x);
         rr[b] = __float_as_int(__fadd_rn(x, 12582912.0f)) - zoff;
@@ -78,12 +78,13 @@ __device__ __forceinline__ void store_chunk16(const EpiArgs& p, int row, int col
     if (MODE == 1 && p.fast) {
         const int32_t zoff = 0x4B400000 - p.zp_c;
         const float floor_x = p.relu ? 0.0f : -8388608.0f;
+        const uint32_t nrowsum = 0u - (uint32_t)rowsum;  // adj = v + c + zp_b * (-rowsum)
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             int4 r4[4];
 #pragma unroll
             for (int b = 0; b < 4; ++b) r4[b] = __ldg(recs + w * 4 + b);
-            packed[w] = requant4_f32_fast(v + w * 4, r4, rowsum, zoff, floor_x);
+            packed[w] = requant4_f32_fast(v + w * 4, r4, nrowsum, zoff, floor_x);
         }
     } else {
 #pragma unroll

@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 // rounding + saturating pack (exact; see conv_tc.cu epi_f32_fast)
                 const int32_t zoff = 0x4B400000 - p.zp_c;
                 const float floor_x = p.relu ? 0.0f : -8388608.0f;
+                const uint32_t nrowsum = 0u - (uint32_t)rowsum;  // once per row, not per value
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     int32_t rr[4];
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                     for (int b = 0; b < 4; ++b) {
                         const int j = w * 4 + b;
                         const int4 r4 = recs[h * 16 + j];
-                        const int32_t adj = (int32_t)(v[j] + (uint32_t)r4.x - (uint32_t)r4.y * (uint32_t)rowsum);
+                        const int32_t adj = (int32_t)(v[j] + ((uint32_t)r4.x + (uint32_t)r4.y * nrowsum));
                         float x = __fmul_rn(__int2float_rn(adj), __int_as_float(r4.z));
                         x = fmaxf(x, floor_x);
                         rr[b] = __float_as_int(__fadd_rn(x, 12582912.0f)) - zoff;
