@@ -390,27 +390,19 @@ struct Dw2Layout {
 };
 __host__ __device__ inline Dw2Layout dw2_layout(int wp) {
     Dw2Layout L;
-    L.halo_off = 1024;  // front guard: the first tap's window starts one position early
+    L.halo_off = 1024;  // (front guard; the 64-channel kernel's windows start at the halo)
     L.halo_stride = align_up((R2 + 2) * wp * CB + 2048, 1024);  // + tail guard (garbage rows run past the end)
     L.b_off = L.halo_off + NB2 * L.halo_stride;
     L.corr_off = L.b_off + 9 * KG * 2048;  // B: [tap][K-group][K half][64 rows][16 B]
     L.mult_off = L.corr_off + 16 * CB * 4;  // [16 classes][64] int32: cterm + border correction
-    // output tiles for the TMA store, double-buffered: [R2 rows][W][64 B], SWIZZLE_64B
+    // per epilogue warp, double-buffered: its 32 positions x 32 channels
+    // (32 rows of 32 B, SWIZZLE_32B) for its own TMA store
     L.out_off = align_up(L.mult_off + CB * 4, 1024);
-    L.out_stride = align_up(R2 * (wp - 2) * CB, 1024);
-    L.bar_off = L.out_off + 2 * L.out_stride;
+    L.out_stride = 2 * 1024;  // per warp
+    L.bar_off = L.out_off + EPI64 * L.out_stride;
     L.tmemptr_off = L.bar_off + (2 * NB2 + 4) * 8;
     L.total = L.tmemptr_off + 16 + 1024;
     return L;
-}
-
-// zero 16 TMEM columns of this warp's 32 lanes
-__device__ __forceinline__ void tmem_st_zero16(uint32_t taddr) {
-    const uint32_t z = 0;
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
-        "r"(z)
-        : "memory");
 }
 
 __host__ __device__ inline uint64_t kmajor_swz64_desc(uint32_t addr) {
@@ -503,16 +495,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     const uint32_t tmem_base = *tmem_ptr;
     const uint32_t halo_bytes = (uint32_t)((R2 + 2) * p.wp * CB);
     // TMEM per accumulator buffer: [K-group j][slot 0: output row r0 + 1 | slot 1: row r0] x 64
-    // columns (32 sum x*w, 32 -zp_w * sum x).  Slot 0 is first written by an
-    // accumulating MMA, so it starts zeroed and the epilogue re-zeroes it after reading.
-    if (warp < EPI64 && (warp / 4) / KG == 1) {
-        const uint32_t zb = tmem_base + ((uint32_t)((warp % 4) * 32) << 16) + (uint32_t)(((warp / 4) % KG) * 128);
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) tmem_st_zero16(zb + (uint32_t)(a * 256 + q4 * 16));
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
+    // columns (32 sum x*w, 32 -zp_w * sum x).  Each slot is initialised by its
+    // own N = 64 MMA group before the N = 128 MMAs accumulate into both.
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -550,7 +534,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
             ptx::mbar_wait(full_bar(b), ph);
             ptx::tc_fence_after();
-            const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride - (uint32_t)CB) >> 4);
+            const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride) >> 4);  // TMEM lane m = output column m
             if (ptx::elect_one()) {
                 dw_stamp(p, 1, (k - cta_in) / ctas);
                 // halo row i = input row r0 - 1 + i feeds output row r0 + 1 with
@@ -559,19 +543,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 //   i = 1: r0+1 (kh 0), r0 (kh 1)  N = 128 into slots 0-1
                 //   i = 2: r0+1 (kh 1), r0 (kh 2)  N = 128 into slots 0-1
                 //   i = 3: r0+1 (kh 2)             N = 64 into slot 0
+                // issued i = 3, 0, 1, 2: the two N = 64 groups initialise their
+                // slots (kw = 0 overwrites), so the N = 128 MMAs that accumulate
+                // into both slots never need a zeroed slot
 #pragma unroll
-                for (int i = 0; i < R2 + 2; ++i)
+                for (int ii = 0; ii < R2 + 2; ++ii)
 #pragma unroll
                     for (int kw = 0; kw < 3; ++kw)
 #pragma unroll
                         for (int j = 0; j < KG; ++j) {
+                            const int i = (ii + 3) % 4;
                             const uint64_t ad = ahalo + (uint64_t)i * row16 + (uint64_t)kw * pos16 + 2u * j;
                             const uint64_t bd = b0 + (uint64_t)((kw * KG + j) * 384);
                             const uint32_t d = tmem_base + (uint32_t)(acc * 256 + j * 128);
                             if (i == 0) ptx::mma_i8(d + 64, ad, bd, idesc64, kw != 0);
                             if (i == 1) ptx::mma_i8(d, ad, bd, idesc128, 1);
                             if (i == 2) ptx::mma_i8(d, ad, bd + 64, idesc128, 1);
-                            if (i == 3) ptx::mma_i8(d, ad, bd + 128, idesc64, 1);
+                            if (i == 3) ptx::mma_i8(d, ad, bd + 128, idesc64, kw != 0);
                         }
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
@@ -594,31 +582,29 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         // (warp % 4); thread = one position.  16 warps (4 per SM sub-partition)
         // keep the TMEM-load latency covered.
         const int ew = warp, quarter = warp % 4, r = (ew / 4) / KG, j = (ew / 4) % KG;
-        const int m = quarter * 32 + lane, ocol = m - 1;
+        const int ocol = quarter * 32 + lane;  // TMEM lane = output column (lanes >= W: clipped by the store)
         const float2 magic2 = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23 (cterm carries its bit pattern)
         const float2 nmagic2 = make_float2(-12582912.0f, -12582912.0f);
         const float floor_x = p.lo == 0.0f ? 0.0f : -8388608.0f;  // ReLU: 0; else -2^23 (see conv_tc.cu)
         const int32_t zoff = 0x4B400000 - p.zp_c;
-        // the unit's 2 x W x 64 output bytes go to a shared-memory tile and out
-        // with one 4-D TMA store (64-byte rows, like the halo) instead of four
-        // 16-byte stores per thread scattered at the C-byte position stride
-        const bool storer = ew == 0 && lane == 0;
+        // each warp stages its 32 positions x 32 channels (1 KB, double
+        // buffered) and stores them with its own TMA store: no CTA-wide
+        // barrier per unit (positions outside the image are clipped by the map)
+        const uint32_t stg0 = ptx::smem_u32(smem + L.out_off + ew * L.out_stride);
         int acc = 0;
         uint32_t aph = 0;
         int ui = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas, ++ui) {
             const int n = k / p.rb2, oh0 = (k % p.rb2) * R2, oh = oh0 + r;
-            const bool valid = oh < p.h && ocol >= 0 && ocol < p.w;
             const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
-            uint8_t* tile = smem + L.out_off + (ui & 1) * L.out_stride;
+            const uint32_t stg = stg0 + (uint32_t)((ui & 1) * 1024);
             // the store issued from this buffer two units ago has read it
-            if (storer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI64) : "memory");
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
             if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
             const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + j * 128 + (1 - r) * 64);
-            const int q = r * p.w + ocol;  // 64-byte row of the tile (SWIZZLE_64B: chunk ^= (q >> 1) & 3)
             // all 32 channels of this warp's tile out of TMEM first, then hand the
             // accumulator buffer back to the MMA warp before the requant math
             uint32_t vw[2][16], vz[2][16];
@@ -628,11 +614,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(32 + hh * 16), vz[hh]);
             }
             ptx::tmem_ld_wait();
-            if (r == 1) {  // slot 0 must be zero before the accumulating MMAs of the buffer's next unit
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) tmem_st_zero16(lane_base + (uint32_t)(q4 * 16));
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
@@ -663,30 +644,29 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                     w4[g] = pack_sat_u8(__float_as_int(x01.y) - zoff, __float_as_int(x01.x) - zoff,
                                         pack_sat_u8(__float_as_int(x23.y) - zoff, __float_as_int(x23.x) - zoff, 0u));
                 }
-                if (ocol >= 0 && ocol < p.w) {
-                    uint4* row16 = reinterpret_cast<uint4*>(tile + (size_t)q * 64);
-                    row16[(2 * j + hh) ^ ((q >> 1) & 3)] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                }
+                // SWIZZLE_32B staging row of 32 B per position: chunk ^= (row >> 2) & 1
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 stg + (uint32_t)(lane * 32 + ((hh ^ ((lane >> 2) & 1)) * 16))),
+                             "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3])
+                             : "memory");
             }
-            (void)valid;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile writes -> TMA
-            asm volatile("bar.sync 2, %0;" ::"n"(32 * EPI64) : "memory");
-            if (storer) {
-                // rows past H are clipped by the tensor map
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging writes -> TMA
+            __syncwarp();
+            if (lane == 0) {
                 asm volatile(
                     "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
                         reinterpret_cast<uint64_t>(&tmap_y)),
-                    "r"(c0), "r"(0), "r"(oh0), "r"(n), "r"(ptx::smem_u32(tile))
+                    "r"(c0 + 32 * j), "r"(quarter * 32), "r"(oh), "r"(n), "r"(stg)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                dw_stamp(p, 4, ui);
+                if (ew == 0) dw_stamp(p, 4, ui);
             }
             if (++acc == 2) {
                 acc = 0;
                 aph ^= 1;
             }
         }
-        if (storer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // smem stays valid until stored
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // smem stays valid until stored
     }
 
     __syncwarp();
@@ -730,12 +710,13 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
             CU_TENSOR_MAP_INTERLEAVE_NONE, tc64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    // output map (64-channel kernel): TMA store of [R2 rows][W][64 ch] tiles
+    // output map (64-channel kernel): per-warp TMA stores of 32 channels x 32 positions
     CUtensorMap tmap_y;
     if (tc64) {
-        cuuint32_t boxy[4] = {(cuuint32_t)CB, (cuuint32_t)w, (cuuint32_t)R2, 1};
+        // per epilogue warp: 32 channels x 32 positions of one output row
+        cuuint32_t boxy[4] = {32, 32, 1, 1};
         if (enc(&tmap_y, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, y, dims, strides, boxy, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
