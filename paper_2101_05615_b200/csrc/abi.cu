@@ -69,8 +69,8 @@ cudaError_t work_slot_prepare(int device) {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     int* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, sizeof(int) * 2 * kWorkSlots);
-    if (e == cudaSuccess && (e = cudaMemset(p, 0, sizeof(int) * 2 * kWorkSlots)) == cudaSuccess)
+    cudaError_t e = cudaMalloc(&p, sizeof(int) * kWorkSlotInts * kWorkSlots);
+    if (e == cudaSuccess && (e = cudaMemset(p, 0, sizeof(int) * kWorkSlotInts * kWorkSlots)) == cudaSuccess)
         e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -85,7 +85,7 @@ int* work_slot(int device) {
     if (device < 0 || device >= 64) return nullptr;
     int* b = __atomic_load_n(&g_work_ring[device].base, __ATOMIC_ACQUIRE);
     if (!b) return nullptr;
-    return b + 2 * (g_work_ring[device].next.fetch_add(1, std::memory_order_relaxed) % kWorkSlots);
+    return b + kWorkSlotInts * (g_work_ring[device].next.fetch_add(1, std::memory_order_relaxed) % kWorkSlots);
 }
 
 bool pdl_enabled() {

@@ -76,7 +76,7 @@ struct CvParams {
     int img_prefetch; // operand image built by an earlier call: load it before griddepcontrol.wait
     void* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): CTA 0 per-unit stamps, else null
-    int* work;          // {claim, done} counters of this launch's work slot, or null: static schedule
+    int* work;          // this launch's work slot (claim counters + done, q8g_internal.cuh), or null: static schedule
     int nstatic;        // static units per CTA before dynamic claiming
 };
 
@@ -341,6 +341,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         __syncwarp();
         const uint32_t ring = base + L.ring_off;
         int i = 0;
+        // dynamic units: group g = blockIdx % kWorkGroups claims units
+        // nstatic * grid + g + kWorkGroups * c from its own counter
+        const int wg = (int)blockIdx.x % kWorkGroups;
         for (;; ++i) {
             int u = (int)blockIdx.x + i * (int)gridDim.x;
             if (p.work && i >= p.nstatic) {
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                     const int j = i - lead;
                     ptx::mbar_wait(empty_bar(j % p.nbuf), (uint32_t)(j / p.nbuf) & 1u);
                 }
-                if (lane == 0) u = p.nstatic * (int)gridDim.x + atomicAdd(p.work, 1);
+                if (lane == 0) u = p.nstatic * (int)gridDim.x + wg + kWorkGroups * atomicAdd(p.work + 8 * wg, 1);
                 u = __shfl_sync(0xffffffffu, u, 0);
             }
             if (u >= p.units) break;
@@ -374,9 +377,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                 // every CTA has made its last claim when done reaches the grid
                 // size: the last one zeroes the slot for its next use
                 __threadfence();
-                if (atomicAdd(p.work + 1, 1) == (int)gridDim.x - 1) {
-                    atomicExch(p.work, 0);
-                    atomicExch(p.work + 1, 0);
+                if (atomicAdd(p.work + kWorkDone, 1) == (int)gridDim.x - 1) {
+                    for (int g = 0; g < kWorkGroups; ++g) atomicExch(p.work + 8 * g, 0);
+                    atomicExch(p.work + kWorkDone, 0);
                 }
             }
         }

@@ -258,14 +258,20 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
 
 int sm_count(int device);
 // Dynamic work claiming for persistent kernels (conv3x3_tc): a per-device
-// ring of kWorkSlots zeroed {claim, done} int pairs.  Each launch takes the
-// next slot; its CTAs claim units with atomicAdd on slot[0] and the last CTA
-// to finish (slot[1] reaching gridDim) zeroes both for the slot's next use
-// kWorkSlots launches later (or the same captured graph node's next replay,
-// which is stream-ordered after this one).  work_slot_prepare allocates the
-// ring (not allowed under stream capture); work_slot returns nullptr when it
-// is not allocated, and the kernel then falls back to its static schedule.
+// ring of kWorkSlots zeroed slots of kWorkSlotInts ints: kWorkGroups claim
+// counters, one per 32-byte sector (a CTA claims from counter blockIdx %
+// kWorkGroups, so the atomics of one launch spread over kWorkGroups L2
+// sectors), and a done counter at kWorkDone.  Each launch takes the next slot;
+// the last CTA to finish (done reaching gridDim) zeroes the slot for its next
+// use kWorkSlots launches later (or the same captured graph node's next
+// replay, which is stream-ordered after this one).  work_slot_prepare
+// allocates the ring (not allowed under stream capture); work_slot returns
+// nullptr when it is not allocated, and the kernel then falls back to its
+// static schedule.
 constexpr int kWorkSlots = 1024;
+constexpr int kWorkGroups = 8;
+constexpr int kWorkDone = 8 * kWorkGroups;
+constexpr int kWorkSlotInts = 8 * kWorkGroups + 8;
 cudaError_t work_slot_prepare(int device);
 int* work_slot(int device);
 // programmatic dependent launch for the tensor-core kernels (env Q8G_PDL=0
