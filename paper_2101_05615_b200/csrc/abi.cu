@@ -793,6 +793,7 @@ struct HostPipeSpec {
     uint8_t* out_host;
     size_t out_pitch, out_width, out_dpitch;
     int units, chunk;
+    bool ramp = false;  // chunk sizes c/4, c/2, c, ..., c/2, c/4 (short first H2D and last D2H)
 };
 
 template <class F>
@@ -831,9 +832,37 @@ int run_host_pipeline(int device, cudaStream_t s, const HostPipeSpec& sp, F comp
     // before this call (a previous call is complete: calls are synchronous)
     if ((e = cudaEventRecord(hp.done, s)) != cudaSuccess || (e = cudaStreamWaitEvent(hp.h2d, hp.done, 0)) != cudaSuccess)
         return cuda_fail(e, "host pipeline ordering");
+    // with sp.ramp chunk sizes ramp up and down (c/4, c/2, c, ..., c, c/2, c/4):
+    // the first H2D and the last D2H run with nothing to overlap, so they are
+    // kept short (C2 host call 1.81 -> 1.73 ms; not used for the conv paths,
+    // whose smallest chunks would leave most SMs idle)
+    int bounds[kMaxChunks + 1];
+    int nch = 0;
+    {
+        const int q = chunk / 4 > 0 ? chunk / 4 : 1, h = chunk / 2 > 0 ? chunk / 2 : 1;
+        const bool ramp = sp.ramp && sp.units >= 4 * chunk && (sp.units + chunk - 1) / chunk + 4 <= kMaxChunks;
+        bounds[nch++] = 0;
+        int u = 0;
+        auto push = [&](int len) {
+            u = u + len < sp.units ? u + len : sp.units;
+            if (u > bounds[nch - 1]) bounds[nch++] = u;
+        };
+        if (ramp) {
+            push(q);
+            push(h);
+            while (sp.units - u > chunk + h + q) push(chunk);
+            const int rest = sp.units - u;  // (h + q, chunk + h + q]: split it c', h, q
+            push(rest - h - q);
+            push(h);
+            push(q);
+        } else {
+            while (u < sp.units) push(chunk);
+        }
+        nch -= 1;  // chunks
+    }
     int rc = Q8G_OK, i = 0;
-    for (int u0 = 0; u0 < sp.units && rc == Q8G_OK; u0 += chunk, ++i) {
-        const int u1 = u0 + chunk < sp.units ? u0 + chunk : sp.units;
+    for (; i < nch && rc == Q8G_OK; ++i) {
+        const int u0 = bounds[i], u1 = bounds[i + 1];
         const size_t n = (size_t)(u1 - u0);
         uint8_t* din = hp.in + sp.in_dpitch * u0;
         uint8_t* dout = hp.out + sp.out_dpitch * u0;
@@ -895,7 +924,7 @@ static int gemm_host(const uint8_t* a_host, int m, int k, int lda, const q8g_pac
         // pair tile), copies overlapped with the GEMM of the previous chunk
         HostPipeSpec sp{a_host + (size_t)row_begin * lda, (size_t)lda, (size_t)k, (size_t)lda_d,
                         reinterpret_cast<uint8_t*>(c_host + (size_t)row_begin * ldc), sizeof(OutT) * ldc,
-                        sizeof(OutT) * pb->n, sizeof(OutT) * ldc_d, rows, host_chunk_rows(rows)};
+                        sizeof(OutT) * pb->n, sizeof(OutT) * ldc_d, rows, host_chunk_rows(rows), true};
         return run_host_pipeline(pb->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
             return gemm_common(din, u1 - u0, k, lda_d, pb, raw ? nullptr : ep, nullptr, dout, ldc_d, 0, u1 - u0,
                                nullptr, s, raw);
