@@ -341,8 +341,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 1 && leader) {
         // ------------------------------------------------ MMA issuer (leader)
         // Per tile the (k block, half) items run k-block-interleaved, except
-        // that the last `de` k blocks issue all their half-0 MMAs before their
-        // half-1 MMAs and the next tile's first `ds` k blocks do the same: the
+        // that the last `de` k blocks (default 4) issue all their half-0 MMAs
+        // before their half-1 MMAs and the next tile's first `ds` k blocks
+        // (default 0) do the same: the
         // half-0 accumulator is complete de half-blocks before half 1, and the
         // next tile needs half 1 back only (de + ds) half-blocks (x 512 MMA
         // cycles) after half 0 was full -- time for the epilogue to drain,
@@ -717,8 +718,10 @@ cudaError_t launch_tc2w(const GemmArgs& g, cudaStream_t s) {
         // boundary) and <= nkb
         static int de0 = -1, ds0 = -1;
         if (de0 < 0) {
-            de0 = 2;
-            ds0 = 2;
+            // C2 (bench.py, 3 interleaved runs each): 4,0 161.5-161.7 us,
+            // 2,2 162.8-163.0, 3,1 163.3-163.4, 3,0 163.3-163.5, 0,4 163.2-163.3
+            de0 = 4;
+            ds0 = 0;
             const char* e = getenv("Q8G_TC2W_SKEW");  // "de,ds" (A/B experiments)
             if (e) sscanf(e, "%d,%d", &de0, &ds0);
         }
