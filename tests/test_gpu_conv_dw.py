@@ -142,6 +142,28 @@ def test_conv3x3_concurrent_first_use_on_two_streams(cuda, orc):
         assert (y.cpu().numpy().reshape(-1, 64) == exp).all()
 
 
+def test_conv3x3_work_slot_ring_wraps(cuda, orc):
+    """The implicit-GEMM conv claims its tail units from a per-launch work slot
+    (a 1024-slot ring per device whose last CTA re-zeroes the slot).  1100
+    launches alternating over two streams wrap the ring; every launch must
+    still cover every unit exactly once (outputs equal to the oracle)."""
+    cc = configs.conv_case(orc, 6, 20, 20, 64, 64, seed=33)
+    pw = q8.prepack_conv3x3_weights(cc.w)
+    _, exp = conv_oracle(orc, cc)
+    pipe = conv_pipeline(cc, 64)
+    xd = dev(cc.x)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ys = [torch.zeros((6, 20, 20, 64), dtype=torch.uint8, device="cuda") for _ in range(4)]
+    for i in range(1100):
+        y = ys[i % 4]
+        if i >= 1096:
+            y.fill_(0)  # the last launch on each buffer starts from zeros
+        q8.execute_conv3x3(xd, pw, y, pipe, stream=streams[i % 2])
+    torch.cuda.synchronize()
+    for y in ys:
+        assert (y.cpu().numpy().reshape(-1, 64) == exp).all()
+
+
 def dw_filter(dc: configs.DwCase):
     rp = q8.RequantParams(multiplier=1.0, zp_a=dc.zp_a, zp_c=dc.zp_c, k_total=9, bias=dc.bias,
                           zp_b_per_channel=dc.zp_w, multiplier_f32_per_channel=dc.mult_f32,
@@ -193,6 +215,25 @@ def test_dwconv_tc_edge_shapes_vs_oracle(cuda, orc, shape, relu, zp_c, fam):
             q8.execute_dwconv3x3(xd, f, y2, image_begin=i0, image_end=i1)
         torch.cuda.synchronize()
         assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("shape", [(3, 6, 112, 256), (3, 5, 33, 64)])
+def test_dwconv_tc64_shard_leaves_other_images_untouched(cuda, orc, shape):
+    """The 64-channel kernel writes through per-warp TMA stores of 32
+    positions x 32 channels, clipped by the output tensor map: convolving
+    image range [1, 2) must write exactly image 1 -- no byte of images 0 / 2
+    and no position past W."""
+    nb, h, w, c = shape
+    dc = configs.dw_case(orc, nb, h, w, c, seed=5 + w)
+    exp, _ = orc.dwconv3x3(dc.x, dc.zp_a, dc.w, dc.zp_w, dc.bias, dc.mult_f32, dc.zp_c, dc.relu)
+    before = q8.launch_stats()["dw_tc"]
+    y = torch.full(shape, 0xA5, dtype=torch.uint8, device="cuda")
+    q8.execute_dwconv3x3(dev(dc.x), dw_filter(dc), y, image_begin=1, image_end=2)
+    torch.cuda.synchronize()
+    assert q8.launch_stats()["dw_tc"] == before + 1
+    yh = y.cpu().numpy()
+    assert (yh[1] == exp[1]).all()
+    assert (yh[0] == 0xA5).all() and (yh[2] == 0xA5).all()
 
 
 # the FMA-pipe kernel forced (Q8G_DW_FMA=1) on shapes the tensor-core kernel
