@@ -62,6 +62,7 @@ struct DwParams {
     int nblk;                  // c / 64
     int rb2;                   // ceil(h / 2)
     int units_blk;             // nb * rb2 units per channel block
+    int nb2;                   // 64-channel kernel: halo buffers
     uint8_t* y;
     unsigned long long* trace;  // debug (Q8G_TC_TRACE): per-unit stamps of CTA 0, else null
 };
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
 // (N = 64), so D = sum_t x_t*w_t (columns 0-31) and -zp_w*sum_t x_t (32-63).
 constexpr int CB = 64;      // channels per block: halo row bytes (SWIZZLE_64B)
 constexpr int R2 = 2;       // output rows per unit, one 128-position M tile each
-constexpr int NB2 = 4;      // halo buffers
+constexpr int NB2 = 5;      // halo buffers at most (p.nb2, dw2_nbuf: 3 by default)
 constexpr int KG = CB / 32; // K-groups of 32 channels
 constexpr int N2 = 64;      // MMA N: 32 outputs + 32 zero-point columns
 constexpr int EPI64 = 4 * R2 * KG;  // epilogue warps: (row, K-group) x TMEM lane quarter
@@ -388,11 +389,11 @@ constexpr int EPI64 = 4 * R2 * KG;  // epilogue warps: (row, K-group) x TMEM lan
 struct Dw2Layout {
     int halo_off, halo_stride, b_off, corr_off, mult_off, out_off, out_stride, bar_off, tmemptr_off, total;
 };
-__host__ __device__ inline Dw2Layout dw2_layout(int wp) {
+__host__ __device__ inline Dw2Layout dw2_layout(int wp, int nb2) {
     Dw2Layout L;
     L.halo_off = 1024;  // (front guard; the 64-channel kernel's windows start at the halo)
-    L.halo_stride = align_up((R2 + 2) * wp * CB + 2048, 1024);  // + tail guard (garbage rows run past the end)
-    L.b_off = L.halo_off + NB2 * L.halo_stride;
+    L.halo_stride = align_up((R2 + 2) * wp * CB + 1024, 1024);  // + tail guard: the last row's windows read 16 positions past it
+    L.b_off = L.halo_off + nb2 * L.halo_stride;
     L.corr_off = L.b_off + 9 * KG * 2048;  // B: [tap][K-group][K half][64 rows][16 B]
     L.mult_off = L.corr_off + 16 * CB * 4;  // [16 classes][64] int32: cterm + border correction
     // per epilogue warp, double-buffered: its 32 positions x 32 channels
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     const uint32_t base = (raw_addr + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base - raw_addr);
-    const Dw2Layout L = dw2_layout(p.wp);
+    const Dw2Layout L = dw2_layout(p.wp, p.nb2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t bar0 = base + L.bar_off;
     auto full_bar = [&](int b) { return bar0 + 8u * b; };
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     if (warp == W_PROD && lane == 0) {
         ptx::prefetch_tmap(&tmap_x);
         ptx::prefetch_tmap(&tmap_y);
-        for (int b = 0; b < NB2; ++b) {
+        for (int b = 0; b < p.nb2; ++b) {
             ptx::mbar_init(full_bar(b), 1);
             ptx::mbar_init(empty_bar(b), 1);
         }
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     float* mult_s = reinterpret_cast<float*>(smem + L.mult_off);
     for (int i = threadIdx.x; i < CB; i += blockDim.x) mult_s[i] = p.mult[c0 + i];
     for (int i = threadIdx.x; i < 64; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
-    for (int b = 0; b < NB2; ++b) {
+    for (int b = 0; b < p.nb2; ++b) {
         const int hb = (R2 + 2) * p.wp * CB;
         uint4* g = reinterpret_cast<uint4*>(smem + L.halo_off + b * L.halo_stride + hb);
         for (int i = threadIdx.x; i < (L.halo_stride - hb) / 16; i += blockDim.x) g[i] = make_uint4(0, 0, 0, 0);
@@ -516,7 +517,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 dw_stamp(p, 0, (k - cta_in) / ctas);
             }
             __syncwarp();
-            if (++b == NB2) {
+            if (++b == p.nb2) {
                 b = 0;
                 ph ^= 1;
             }
@@ -566,7 +567,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 dw_stamp(p, 2, (k - cta_in) / ctas);
             }
             __syncwarp();
-            if (++b == NB2) {
+            if (++b == p.nb2) {
                 b = 0;
                 ph ^= 1;
             }
@@ -678,9 +679,22 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     }
 }
 
+// halo buffers of the 64-channel kernel: 3.  Fewer buffers keep the block's
+// CTAs in step on adjacent rows (shared halo rows hit in L2): C4 with 2 / 3 /
+// 4 / 5 buffers 87.8 / 59.6 / 63.0 / 67.9 us (Q8G_DW_NBUF, A/B)
+int dw2_nbuf(int wp) {
+    static const int env = [] {
+        const char* e = getenv("Q8G_DW_NBUF");
+        return e ? std::atoi(e) : 0;
+    }();
+    int nb = env > 0 ? std::max(2, std::min(NB2, env)) : 3;
+    while (nb > 2 && dw2_layout(wp, nb).total > 232448) --nb;
+    return nb;
+}
+
 bool dw_tc64_ok(int w, int c) {
     static const bool off = getenv("Q8G_DW_TC16") != nullptr;  // A/B switch: force the 16-channel kernel
-    return !off && c % CB == 0 && w + 2 <= 128 && dw2_layout(w + 2).total <= 232448;
+    return !off && c % CB == 0 && w + 2 <= 128 && dw2_layout(w + 2, dw2_nbuf(w + 2)).total <= 232448;
 }
 
 }  // namespace
@@ -744,6 +758,7 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
     p.nblk = c / CB;
     p.rb2 = (h + R2 - 1) / R2;
     p.units_blk = nb * p.rb2;
+    p.nb2 = dw2_nbuf(p.wp);
     int dev = 0;
     cudaGetDevice(&dev);
     if (tc64) {
@@ -758,7 +773,7 @@ cudaError_t launch_dwconv3x3_tc(const uint8_t* x, int nb, int h, int w, int c, c
         if (per_blk < 1) per_blk = 1;
         if (per_blk > p.units_blk) per_blk = p.units_blk;
         const cudaError_t e = launch_with_pdl(dwconv_tc64_kernel, dim3(per_blk * p.nblk), dim3(128 + 32 * EPI64),
-                                              dw2_layout(p.wp).total, s, tmap, tmap_y, p);
+                                              dw2_layout(p.wp, p.nb2).total, s, tmap, tmap_y, p);
         count_launch(kFamDwTc);
         return e;
     }
