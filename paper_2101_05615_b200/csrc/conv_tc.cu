@@ -615,8 +615,11 @@ CvParams make_params(const ConvArgs& a) {
     p.fast = (!a.raw && a.ep->fast_f32) ? 1 : 0;
     p.y = a.y;
     p.trace = tc_trace_buffer_ptr();
-    // as many halo buffers as fit next to the operand image (>= 2)
-    int maxbuf = MAX_BUF;
+    // 5 halo buffers (fewer if they do not fit next to the operand image, >= 2).
+    // C3 over Q8G_CONV_NBUF = 2..8: 10.4 / 10.8 / 11.1 / 9.0-9.1 / 9.3 / 9.35-9.4
+    // / 9.4-9.5 us; a CTA running further ahead of its neighbours loses the
+    // L2 sharing of their common halo rows (as in the depthwise kernel)
+    int maxbuf = 5;
     if (const char* e = getenv("Q8G_CONV_NBUF")) maxbuf = std::max(2, std::min(MAX_BUF, std::atoi(e)));
     for (p.nbuf = maxbuf; p.nbuf > 2 && cv_layout(p).total > 232448; --p.nbuf) {
     }
