@@ -14,7 +14,7 @@
 //
 // Cost: the workspace write + read (9C per output pixel) on top of the conv's
 // own traffic, bounded to 256 MB per chunk of images; the GEMM runs at the
-// tensor-core rates of gemm_tc.cu / gemm_tc2.cu / gemm_splitk.cu.
+// tensor-core rates of gemm_tc.cu / gemm_tc2w.cu / gemm_splitk.cu.
 #include <cstdint>
 #include <map>
 #include <mutex>

@@ -1,5 +1,5 @@
 // epilogue.cuh — the fused back-end on the TMEM -> register -> global drain,
-// shared by the large-M GEMM kernels (gemm_tc.cu 1-CTA, gemm_tc2.cu CTA
+// shared by the large-M GEMM kernels (gemm_tc.cu 1-CTA, gemm_tc2w.cu CTA
 // pair): 16 accumulator columns of one output row per call.
 //
 // MODE 0: raw int32 (+ BiasAdd; WriteRawI32, pipeline.hpp:191-198)

@@ -575,7 +575,6 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s) {
     if (tile_kind == kSmallM) return launch_modes<32, 1, 10>(g, s);
     if (tile_kind == kMidM) return launch_modes<128, 2, 6>(g, s);
     if (tc2w_supported(g)) return launch_gemm_tc2w(g, s);  // CTA-pair 256x512 tiles
-    if (tc2_supported(g)) return launch_gemm_tc2(g, s);    // CTA-pair 256x256 tiles
     return launch_modes<256, 1, 4>(g, s);
 }
 

@@ -2,7 +2,8 @@
 // (tcgen05.mma.cta_group::2, two N=256 MMAs per K step sharing A): the
 // BASELINE C2 kernel (M=16384, N=K=4096).
 //
-// Why a wider tile than gemm_tc2.cu (256 x 256): every byte a CTA pulls from
+// Why a 512-column tile (round 1 had 256 x 256 pair tiles, gemm_tc2.cu,
+// removed in round 2): every byte a CTA pulls from
 // L2 into shared memory costs crossbar / die-to-die energy, and C2 runs at
 // the 1 kW power limit (in-kernel clock64 / globaltimer: ~1.5 GHz, not 1.965,
 // tools/c2_clock.py).  Per 128-byte K block a CTA now receives A 16 KB + B
@@ -10,7 +11,7 @@
 // 64, and its shared memory carries 48 KB of TMA writes + 64 KB of MMA reads
 // per 1024 MMA cycles (109 B/clk of the ~128 B/clk port) instead of 128.
 //
-// Same drop-in semantics as gemm_tc2.cu / gemm_tc.cu: engine.hpp:59-169 for
+// Same drop-in semantics as gemm_tc.cu: engine.hpp:59-169 for
 // the contraction, pipeline.hpp:157-210 + quant.hpp:115-133 for the fused
 // requantizing back-end (epilogue.cuh).
 //
@@ -96,7 +97,9 @@ struct Cfg {
 struct Tc2wParams {
     const uint8_t* a;  // not read by the kernel (TMA maps only); kept for traces
     int nkb, n, rows;
-    int num_m_tiles, num_n_tiles;  // pair tiles: 256 rows x 512 columns
+    int num_m_tiles, num_n_tiles;  // pair tiles: 256 rows x 512 columns (the last may hang past np)
+    int np;                        // packed-B columns (a multiple of 256)
+    int b3d;                       // np % 512 != 0: B through the 3-D map (zero columns past np)
     int sched;                     // 1: contiguous ranges per pair, 0: round-robin
     int skew_end, skew_start;      // MMA issue-order skew at tile boundaries (k blocks)
     int tma_out;                   // u8 output through smem staging + TMA stores (tmap_c valid)
@@ -166,6 +169,18 @@ __device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const CUtens
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
+        : "memory");
+}
+
+// packed B through a 3-D map (128 K-bytes, np columns, kp/128 k-blocks): a box
+// of columns past np is zero-filled, so a last 512-column tile over an np that
+// is an odd multiple of 256 reads zeros for its second half
+__device__ __forceinline__ void tma_load_3d_pair_hint(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                                      uint32_t bar_cluster, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster), "l"(policy)
         : "memory");
 }
 
@@ -328,8 +343,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     ptx::tma_load_2d_pair(stage_a(stage), &tmap_a, kb * kKBlock, m0, fb);
 #pragma unroll
                     for (int h = 0; h < NSUB; ++h)
-                        tma_load_2d_pair_hint(stage_b(stage, h), &tmap_b, 0, kb * (p.num_n_tiles * PN) + brow + h * 2 * HN,
-                                              fb, pol_b);
+                        if (p.b3d)
+                            tma_load_3d_pair_hint(stage_b(stage, h), &tmap_b, 0, brow + h * 2 * HN, kb, fb, pol_b);
+                        else
+                            tma_load_2d_pair_hint(stage_b(stage, h), &tmap_b, 0, kb * p.np + brow + h * 2 * HN, fb,
+                                                  pol_b);
                 }
                 __syncwarp();
                 if (++stage == STAGES) {
@@ -496,7 +514,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // MMAs run (all 8 warps are done with the previous tile's)
                 named_bar_sync(1, 256);
                 for (int i = et; i < PN; i += 256) {
-                    const int4 rr = __ldg(reinterpret_cast<const int4*>(p.ea.rec) + ntile * PN + i);
+                    const int4 rr = ntile * PN + i < p.np ? __ldg(reinterpret_cast<const int4*>(p.ea.rec) + ntile * PN + i)
+                                                          : make_int4(0, 0, 0, 0);  // (columns past np: never stored)
                     rc[i] = rr.x;
                     rz[i] = rr.y;
                     rm[i] = rr.z;
@@ -582,19 +601,32 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// packed B (q8g_internal.cuh) as a 2-D u8 tensor of (kp/128 * np) rows of 128
-// bytes, box 128 x 128 rows, no swizzle: the rows are pre-swizzled, so a box
-// lands in shared memory in the tcgen05 K-major SW128 layout
+// packed B (q8g_internal.cuh) as u8 rows of 128 K-bytes, box 128 B x 128
+// columns, no swizzle: the rows are pre-swizzled, so a box lands in shared
+// memory in the tcgen05 K-major SW128 layout.  np % 512 == 0: a 2-D tensor of
+// (kp/128 * np) rows.  Otherwise a 3-D tensor (128 B, np columns, kp/128
+// k-blocks) whose columns past np read as zeros, for the last 512-column
+// tile.  (The 3-D map for every shape measured C2 at 165 us vs 161.6 us and
+// a lower clock: 1575 vs 1615 MHz.)
 bool make_tmap_b(CUtensorMap* m, const q8g_packed_b* pb) {
     auto enc = tmap_encoder();
     if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)kKBlock, (cuuint64_t)(pb->kp / kKBlock) * (cuuint64_t)pb->np};
-    cuuint64_t strides[1] = {(cuuint64_t)kKBlock};
-    cuuint32_t box[2] = {(cuuint32_t)kKBlock, (cuuint32_t)HN};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, pb->data, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (pb->np % PN == 0) {
+        cuuint64_t dims[2] = {(cuuint64_t)kKBlock, (cuuint64_t)(pb->kp / kKBlock) * (cuuint64_t)pb->np};
+        cuuint64_t strides[1] = {(cuuint64_t)kKBlock};
+        cuuint32_t box[2] = {(cuuint32_t)kKBlock, (cuuint32_t)HN};
+        cuuint32_t estr[2] = {1, 1};
+        r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, pb->data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[3] = {(cuuint64_t)kKBlock, (cuuint64_t)pb->np, (cuuint64_t)(pb->kp / kKBlock)};
+        cuuint64_t strides[2] = {(cuuint64_t)kKBlock, (cuuint64_t)pb->np * kKBlock};
+        cuuint32_t box[3] = {(cuuint32_t)kKBlock, (cuuint32_t)HN, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, pb->data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     return r == CUDA_SUCCESS;
 }
 
@@ -710,7 +742,9 @@ cudaError_t launch_tc2w(const GemmArgs& g, cudaStream_t s) {
     p.n = g.pb->n;
     p.rows = g.rows;
     p.num_m_tiles = ceil_div_i(g.rows, 2 * BM);
-    p.num_n_tiles = g.pb->np / PN;
+    p.num_n_tiles = ceil_div_i(g.pb->np, PN);
+    p.np = g.pb->np;
+    p.b3d = g.pb->np % PN != 0;
     p.sched = env_sched();
     p.tma_out = MODE == 3 ? 1 : 0;
     {
@@ -757,14 +791,15 @@ int tc2w_last_clock(unsigned long long* cycles, unsigned long long* ns) {
     return 0;
 }
 
-// the 512-column pair tile needs N padded to 512 (np % 512 == 0); Q8G_TC2W=0
-// falls back to the 256 x 256 pair kernel (gemm_tc2.cu)
+// every large-M shape (a last 512-column tile past np reads zero weights and
+// stores nothing); Q8G_TC2W=0 falls back to the 1-CTA 256-row kernel
+// (gemm_tc.cu) for A/B
 bool tc2w_supported(const GemmArgs& g) {
     static const bool off = [] {
         const char* e = getenv("Q8G_TC2W");
         return e && e[0] == '0';
     }();
-    return !off && g.pb->np % PN == 0 && tmap_encoder() != nullptr;
+    return !off && tmap_encoder() != nullptr;
 }
 
 cudaError_t launch_gemm_tc2w(const GemmArgs& g, cudaStream_t s) {

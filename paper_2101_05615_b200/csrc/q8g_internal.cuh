@@ -216,11 +216,9 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, int tile_kind, cudaStream_t s);
 bool tc_supported(const GemmArgs& g);
 bool splitk_supported(const GemmArgs& g);
 cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s);
-bool tc2_supported(const GemmArgs& g);
 cudaError_t launch_post(int writer, const int32_t* acc, int ldacc, const uint8_t* a, int lda, int rows, int k, int n,
                         const q8g_sparse_csc* sp, const q8g_epilogue* ep, double dq_scale, int32_t dq_zp, void* out,
                         int ldc, cudaStream_t s);
-cudaError_t launch_gemm_tc2(const GemmArgs& g, cudaStream_t s);
 bool tc2w_supported(const GemmArgs& g);
 int tc2w_last_clock(unsigned long long* cycles, unsigned long long* ns);
 cudaError_t launch_gemm_tc2w(const GemmArgs& g, cudaStream_t s);
