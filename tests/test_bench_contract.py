@@ -53,3 +53,33 @@ def test_reference_arm_other_ranks_silent():
     rc, out, _ = run_bench("--impl", "reference", "--config", "C1", "--steps", "1", "--gpus", "2",
                            env_extra={"RANK": "1", "WORLD_SIZE": "2"})
     assert rc == 0 and out.strip() == ""
+
+
+REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["C2", "C1", "C3", "C4"])
+def test_our_arm_line_on_the_gpu(cfg):
+    """bench.py's own arm on a B200: one JSON line with every contract key, the
+    device value and an end-to-end value through the host-view ABI, our
+    kernels counted in the timed region, and the same config dict the
+    reference arm prints."""
+    rc, out, err = run_bench("--config", cfg, "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-sub",
+                             timeout=600)
+    assert rc == 0, err
+    lines = [ln for ln in out.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in REQUIRED:
+        assert key in d, key
+    assert d["unit"] == "TOPS" and d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3
+    assert d["gpu_launches"] == 3  # one launch of our kernel per step
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    r = d["roofline"]
+    assert r["bound"] == ("tensor" if cfg == "C2" else "hbm") and 0 < r["frac"] < 1 and r["peak"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert d["config"] == bench.config_dict(cfg, 1)
