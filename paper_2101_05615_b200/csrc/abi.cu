@@ -893,6 +893,18 @@ int run_host_pipeline(int device, cudaStream_t s, const HostPipeSpec& sp, F comp
 }
 }  // namespace
 
+// images per chunk of the host-view conv / depthwise pipelines: imgs / parts
+// (Q8G_HOST_CHUNK_IMG overrides, A/B)
+static int host_chunk_images(int imgs, int parts, size_t img_bytes) {
+    (void)img_bytes;
+    static const int env = [] {
+        const char* e = getenv("Q8G_HOST_CHUNK_IMG");
+        return e ? atoi(e) : 0;
+    }();
+    if (env > 0) return env;
+    return std::max(1, (imgs + parts - 1) / parts);
+}
+
 // rows per chunk of the host-view GEMM pipeline (Q8G_HOST_CHUNK overrides, A/B)
 static int host_chunk_rows(int rows) {
     static const int env = [] {
@@ -1264,7 +1276,8 @@ int q8g_conv3x3_u8s8_nhwc_host(const uint8_t* x_host, int nb, int h, int w, int 
     const size_t xi = (size_t)h * w * c, yi = (size_t)h * w * pw->n;
     const int imgs = img_end - img_begin;
     HostPipeSpec sp{x_host + xi * img_begin, xi, xi, xi, y_host + yi * img_begin, yi, yi, yi, imgs,
-                    std::max(1, (imgs + 7) / 8)};
+                    host_chunk_images(imgs, 8, xi)};
+    sp.ramp = (size_t)sp.chunk * xi >= ((size_t)4 << 20);  // (C3: 0.8 MB chunks, no ramp)
     const cudaStream_t s = (cudaStream_t)stream;
     return run_host_pipeline(pw->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
         (void)u0;
@@ -1284,7 +1297,8 @@ int q8g_dwconv3x3_u8s8_nhwc_host(const uint8_t* x_host, int nb, int h, int w, in
     const size_t img = (size_t)h * w * c;
     const int imgs = img_end - img_begin;
     HostPipeSpec sp{x_host + img * img_begin, img, img, img, y_host + img * img_begin, img, img, img, imgs,
-                    std::max(1, (imgs + 15) / 16)};
+                    host_chunk_images(imgs, 8, img)};  // C4 e2e: 4-image chunks 2.48 ms, 2: 2.59, 8: 2.57
+    sp.ramp = (size_t)sp.chunk * img >= ((size_t)4 << 20);  // copies long enough to outweigh per-chunk overhead
     const cudaStream_t s = (cudaStream_t)stream;
     return run_host_pipeline(f->device, s, sp, [&](int u0, int u1, uint8_t* din, uint8_t* dout) {
         (void)u0;
