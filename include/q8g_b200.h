@@ -67,7 +67,9 @@ uint64_t q8g_launch_count(void);
  * [3] GEMM tcgen05 large-M, [4] conv CUDA-core, [5] conv tcgen05,
  * [6] depthwise CUDA-core, [7] depthwise tcgen05, [8] general-pipeline post,
  * [9] conv3x3 im2col (shapes the implicit-GEMM kernel cannot hold; the GEMM
- *     launches count under [2] / [3]) */
+ *     launches count under [2] / [3]), [10] depthwise FMA-pipe,
+ * [11] copy-engine peer copies of q8g_gemm_u8s8_requant_peers (not kernels:
+ *      not in q8g_launch_count) */
 int q8g_launch_stats(uint64_t* counts, int n);
 /* debug (env Q8G_TC_TRACE set): 8 globaltimer stamps per CTA of the last
  * tensor-core GEMM launch; returns the number of CTA records copied.  With
@@ -130,6 +132,23 @@ int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, in
 int q8g_gemm_u8s8_requant(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
                           const q8g_epilogue* ep, uint8_t* c_dev, int ldc, int row_begin,
                           int row_end, q8g_kernel_cache* cache, void* stream);
+/* N-sharded multi-GPU (optional N-sharding; no reference
+ * symbol -- the reference splits only M: engine.hpp:39-47,102-103).  Same as
+ * q8g_gemm_u8s8_requant for one column shard (pb packs B[:, n0:n1] on this
+ * device, ep its columns), and the stripe is ALSO written at each of the
+ * n_peers (0..7) pointers: other devices' C windows at the same shard offset
+ * (UVA device pointers, same ldc), so after every rank has run its shard each
+ * rank holds the whole M x N output -- an all-gather with no separate pass.
+ * The CTA-pair kernel stores each tile to the peers straight from its
+ * staging tile (TMA stores over NVLink, overlapped with the GEMM); other
+ * kernels copy the finished stripe with the copy engines.  Peer access is
+ * enabled on first use.  Completion on the peers is ordered by `stream`:
+ * the caller synchronises the ranks (e.g. a barrier after a stream sync)
+ * before reading the gathered output. */
+int q8g_gemm_u8s8_requant_peers(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                                const q8g_epilogue* ep, uint8_t* c_dev, uint8_t* const* c_peer_dev,
+                                int n_peers, int ldc, int row_begin, int row_end,
+                                q8g_kernel_cache* cache, void* stream);
 /* WriteRawI32 writer (pipeline.hpp:38,191-198); bias_add_dev = optional
  * BiasAdd stage (N int32, device) or NULL */
 int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,

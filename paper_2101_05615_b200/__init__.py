@@ -31,3 +31,4 @@ from .api import (  # noqa: F401
     select_blocking,
 )
 from ._lib import InvalidArgument, Q8GError, launch_count, launch_stats  # noqa: F401
+from .nshard import NShardedGemm, column_shard, execute_gemm_to_peers  # noqa: F401,E402

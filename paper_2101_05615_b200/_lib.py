@@ -90,6 +90,7 @@ _SIGS = [
     ("q8g_kernel_cache_build_count", C.c_uint64, [_P]),
     ("q8g_kernel_cache_tile", _I, [_P, _I, _I, _I, _I, C.POINTER(_I)]),
     ("q8g_gemm_u8s8_requant", _I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P, _P]),
+    ("q8g_gemm_u8s8_requant_peers", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     ("q8g_gemm_u8s8_raw_i32", _I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P, _P]),
     ("q8g_gemm_u8s8_requant_host", _I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P]),
     ("q8g_gemm_u8s8_raw_i32_host", _I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _P]),
@@ -148,7 +149,7 @@ def launch_count() -> int:
 
 
 FAMILIES = ("pack", "gemm_simt", "gemm_tc_small_m", "gemm_tc_large_m", "conv_simt", "conv_tc", "dw_simt",
-            "dw_tc", "post", "conv_im2col", "dw_fma")
+            "dw_tc", "post", "conv_im2col", "dw_fma", "peer_copy")
 
 
 def launch_stats() -> dict:

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <mutex>
+#include <set>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -39,7 +40,7 @@ int cuda_fail(cudaError_t e, const char* what) {
     return Q8G_ECUDA;
 }
 void count_launch(int family) {
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (family != kFamPeerCopy) g_launches.fetch_add(1, std::memory_order_relaxed);
     if (family >= 0 && family < kFamCount) g_family[family].fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -521,7 +522,8 @@ int q8g_kernel_cache_tile(q8g_kernel_cache* kc, int m, int n, int k, int lda, in
 static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed_b* pb,
                        const q8g_epilogue* ep, const int32_t* bias_add, void* c, int ldc,
                        int row_begin, int row_end, q8g_kernel_cache* cache, cudaStream_t s,
-                       bool raw, const uint32_t* a_ready = nullptr, uint32_t a_epoch = 0) {
+                       bool raw, const uint32_t* a_ready = nullptr, uint32_t a_epoch = 0,
+                       uint8_t* const* c_peers = nullptr, int n_peers = 0) {
     if (!pb) return fail(Q8G_EINVAL, "execute_gemm: null packed weight");
     if (k != pb->k) return fail(Q8G_EINVAL, "execute_gemm: A columns must equal the packed weight K");
     if (m < 1 || lda < k || ldc < pb->n || !a || !c)
@@ -549,6 +551,12 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
               : (void*)((uint8_t*)c + (size_t)row_begin * ldc);
     g.a_ready = a_ready;
     g.a_epoch = a_epoch;
+    uint8_t* peers[kMaxPeers];
+    bool peers_written = false;
+    for (int d = 0; d < n_peers; ++d) peers[d] = c_peers[d] + (size_t)row_begin * ldc;
+    g.c_peers = peers;
+    g.n_peers = n_peers;
+    g.peers_written = &peers_written;
     const int kind = resolve_tile(cache ? cache : &process_cache(), g.rows, pb->n, k,
                                   a_is_tma_aligned(g.a, lda));
     cudaError_t e;
@@ -559,6 +567,41 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
         if (e == cudaSuccess) e = launch_gemm_simt(g, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "gemm launch");
+    // kernels without peer stores (small M, non-fast epilogues): the stripe
+    // goes from the local C to each peer by the copy engines, stream-ordered
+    for (int d = 0; d < n_peers && !peers_written; ++d) {
+        e = cudaMemcpy2DAsync(peers[d], (size_t)ldc, g.c, (size_t)ldc, (size_t)pb->n, (size_t)g.rows,
+                              cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "peer copy");
+        count_launch(kFamPeerCopy);
+    }
+    return Q8G_OK;
+}
+
+// peer access from `dev` to the device holding `ptr` (once per pair);
+// Q8G_OK also when ptr is on `dev` itself
+static int enable_peer_access(int dev, const void* ptr) {
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_peers: cudaPointerGetAttributes");
+    if (at.type != cudaMemoryTypeDevice) return fail(Q8G_EINVAL, "gemm_peers: peer output must be device memory");
+    if (at.device == dev) return Q8G_OK;
+    static std::mutex mu;
+    static std::set<std::pair<int, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, at.device})) return Q8G_OK;
+    int can = 0;
+    e = cudaDeviceCanAccessPeer(&can, dev, at.device);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_peers: cudaDeviceCanAccessPeer");
+    if (!can) return fail(Q8G_ENOTSUP, "gemm_peers: no peer access between the devices");
+    DeviceGuard dg(dev);
+    e = cudaDeviceEnablePeerAccess(at.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        e = cudaSuccess;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_peers: cudaDeviceEnablePeerAccess");
+    done.insert({dev, at.device});
     return Q8G_OK;
 }
 
@@ -567,6 +610,23 @@ int q8g_gemm_u8s8_requant(const uint8_t* a_dev, int m, int k, int lda, const q8g
                           int row_end, q8g_kernel_cache* cache, void* stream) {
     return gemm_common(a_dev, m, k, lda, pb, ep, nullptr, c_dev, ldc, row_begin, row_end, cache,
                        (cudaStream_t)stream, false);
+}
+
+int q8g_gemm_u8s8_requant_peers(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
+                                const q8g_epilogue* ep, uint8_t* c_dev, uint8_t* const* c_peer_dev,
+                                int n_peers, int ldc, int row_begin, int row_end, q8g_kernel_cache* cache,
+                                void* stream) {
+    if (n_peers < 0 || n_peers > kMaxPeers) return fail(Q8G_EINVAL, "gemm_peers: 0 to 7 peer outputs");
+    if (n_peers > 0 && !c_peer_dev) return fail(Q8G_EINVAL, "gemm_peers: null peer output list");
+    for (int d = 0; d < n_peers; ++d) {
+        if (!c_peer_dev[d]) return fail(Q8G_EINVAL, "gemm_peers: null peer output");
+        if (pb) {
+            const int st = enable_peer_access(pb->device, c_peer_dev[d]);
+            if (st != Q8G_OK) return st;
+        }
+    }
+    return gemm_common(a_dev, m, k, lda, pb, ep, nullptr, c_dev, ldc, row_begin, row_end, cache,
+                       (cudaStream_t)stream, false, nullptr, 0, c_peer_dev, n_peers);
 }
 
 int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,

@@ -94,6 +94,13 @@ struct Cfg {
     static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
+// TMA store maps of the peer destinations (N-sharded multi-GPU: every tile
+// the epilogue stores locally also goes straight to each peer's C over
+// NVLink, from the same staging tile)
+struct PeerMaps {
+    CUtensorMap m[kMaxPeers];
+};
+
 struct Tc2wParams {
     const uint8_t* a;  // not read by the kernel (TMA maps only); kept for traces
     int nkb, n, rows;
@@ -103,6 +110,7 @@ struct Tc2wParams {
     int sched;                     // 1: contiguous ranges per pair, 0: round-robin
     int skew_end, skew_start;      // MMA issue-order skew at tile boundaries (k blocks)
     int tma_out;                   // u8 output through smem staging + TMA stores (tmap_c valid)
+    int n_peers;                   // MODE 3: peer destinations in PeerMaps (0: local only)
     EpiArgs ea;
     unsigned long long* trace;
 };
@@ -263,7 +271,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 template <int MODE, bool RS>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc2w_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                     const __grid_constant__ CUtensorMap tmap_c, const Tc2wParams p) {
+                     const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ PeerMaps peers,
+                     const Tc2wParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     const uint32_t base = (raw_addr + 1023u) & ~1023u;
@@ -575,7 +584,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         __syncwarp();
                         if (warp == 4 && lane == 0) tw_epi(p, 3 * h + 2 * rd, ti);
-                        if (lane == 0) tma_store_2d(&tmap_c, stg, col0 + rd * 64, mt * 2 * BM + (int)rank * BM + q * 32);
+                        if (lane == 0) {
+                            const int orow = mt * 2 * BM + (int)rank * BM + q * 32;
+                            tma_store_2d(&tmap_c, stg, col0 + rd * 64, orow);
+                            for (int d = 0; d < p.n_peers; ++d) tma_store_2d(&peers.m[d], stg, col0 + rd * 64, orow);
+                        }
                     }
                 } else if (valid) {
 #pragma unroll
@@ -736,6 +749,17 @@ cudaError_t launch_tc2w(const GemmArgs& g, cudaStream_t s) {
     if (!cached_tmap_b(&tb, g.pb)) return cudaErrorInvalidValue;
     memset(&tc, 0, sizeof(tc));
     if (MODE == 3 && !cached_tmap_c(&tc, g.c, g.rows, g.pb->n, g.ldc)) return cudaErrorNotSupported;
+    PeerMaps pm;
+    memset(&pm, 0, sizeof(pm));
+    int n_peers = 0;
+    if (MODE == 3 && g.n_peers > 0) {
+        if (g.n_peers > kMaxPeers) return cudaErrorNotSupported;
+        for (int d = 0; d < g.n_peers; ++d)
+            if ((reinterpret_cast<uintptr_t>(g.c_peers[d]) & 15) != 0 ||
+                !cached_tmap_c(&pm.m[d], g.c_peers[d], g.rows, g.pb->n, g.ldc))
+                return cudaErrorNotSupported;
+        n_peers = g.n_peers;
+    }
     Tc2wParams p;
     p.a = g.a;
     p.nkb = g.pb->kp / kKBlock;
@@ -747,6 +771,7 @@ cudaError_t launch_tc2w(const GemmArgs& g, cudaStream_t s) {
     p.b3d = g.pb->np % PN != 0;
     p.sched = env_sched();
     p.tma_out = MODE == 3 ? 1 : 0;
+    p.n_peers = n_peers;
     {
         // MMA skew: de + ds <= STAGES (the stages held across the tile
         // boundary) and <= nkb
@@ -775,8 +800,9 @@ cudaError_t launch_tc2w(const GemmArgs& g, cudaStream_t s) {
     const int clusters = total < maxc ? total : maxc;
     cfg.gridDim = dim3(2 * clusters);
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, pm, p);
     count_launch(kFamGemmTcLargeM);
+    if (e == cudaSuccess && n_peers > 0 && g.peers_written) *g.peers_written = true;
     return e;
 }
 

@@ -50,7 +50,8 @@ enum KernelFamily : int {
     kFamPost = 8,        // general-pipeline post kernel (post.cu)
     kFamConvIm2col = 9,  // conv3x3 im2col for the GEMM path (conv_im2col.cu)
     kFamDwFma = 10,      // depthwise on the CUDA-core FMA pipes (dwconv_fma.cu)
-    kFamCount = 11
+    kFamPeerCopy = 11,   // copy-engine peer copies of a stripe (gemm_peers fallback; not a kernel)
+    kFamCount = 12
 };
 void count_launch(int family);
 
@@ -207,7 +208,15 @@ struct GemmArgs {
     // makes the stream wait on the flag before launching.  null = A resident.
     const uint32_t* a_ready = nullptr;
     uint32_t a_epoch = 0;
+    // N-sharded multi-GPU (q8g_gemm_u8s8_requant_peers): the same stripe is
+    // also written at each of these pointers (peer devices' C windows, UVA,
+    // same ldc).  A kernel that stores to them itself sets *peers_written;
+    // otherwise the ABI copies dest 0 to them after the launch.
+    uint8_t* const* c_peers = nullptr;
+    int n_peers = 0;
+    bool* peers_written = nullptr;
 };
+constexpr int kMaxPeers = 7;  // peer destinations of one call (8 GPUs of a node)
 // stream memory operations (driver API via cudaGetDriverEntryPoint)
 cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value);
 cudaError_t stream_wait_u32(cudaStream_t s, const uint32_t* addr, uint32_t value);  // until *addr == value
