@@ -529,6 +529,25 @@ void execute_gemm(DeviceView<const uint8_t> a, const PackedWeight& pw, DeviceVie
     }
 }
 
+// N-sharded multi-GPU (optional; no reference counterpart):
+// columns [col0, col0 + pw.n_total) of the output -- pw packs that column
+// shard of B on this device -- go to `out` (this device's whole M x N output)
+// and to every peer output at the same offset (UVA device pointers of buffers
+// with out's leading dimension, up to 7).  See q8g_gemm_u8s8_requant_peers.
+inline void execute_gemm_to_peers(DeviceView<const uint8_t> a, const PackedWeight& pw, DeviceView<uint8_t> out,
+                                  const std::vector<uint8_t*>& peers, int col0, const OutputPipeline& pipeline,
+                                  KernelCache* cache = nullptr, void* stream = nullptr) {
+    if (a.cols != pw.k_total) throw std::invalid_argument("execute_gemm: A columns must equal the packed weight K");
+    if (out.rows != a.rows || col0 < 0 || col0 + pw.n_total > out.cols)
+        throw std::invalid_argument("execute_gemm_to_peers: shard columns must lie inside out");
+    detail::check_writer_matches<uint8_t>(pipeline);
+    std::vector<uint8_t*> shifted;
+    for (uint8_t* p : peers) shifted.push_back(p + col0);
+    check(q8g_gemm_u8s8_requant_peers(a.data, a.rows, a.cols, a.ld, pw.handle(), pipeline.epilogue(pw),
+                                      out.data + col0, shifted.data(), (int)shifted.size(), out.ld, 0, a.rows,
+                                      cache ? cache->handle() : nullptr, stream));
+}
+
 // ------------------------------------------------------------------ conv / depthwise (new entry points)
 
 // weights [3][3][C][OC] int8 (host) -> packed K = 9C x N = OC, with the

@@ -418,6 +418,22 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
     return d;
 }
 
+// (image, row block) of a CTA's units k = first, first + step, ...: stepped
+// incrementally (no integer division per unit in the role loops)
+struct UnitWalk {
+    int n, rb, dn, drb, rb2;
+    __device__ UnitWalk(int first, int step, int rb2_) : n(first / rb2_), rb(first % rb2_), dn(step / rb2_),
+                                                         drb(step % rb2_), rb2(rb2_) {}
+    __device__ __forceinline__ void next() {
+        n += dn;
+        rb += drb;
+        if (rb >= rb2) {
+            rb -= rb2;
+            ++n;
+        }
+    }
+};
+
 __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     dwconv_tc64_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                        const DwParams p) {
@@ -507,8 +523,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         ptx::griddep_wait();  // x may be the previous grid's output
         int b = 0;
         uint32_t ph = 0;
-        for (int k = cta_in; k < p.units_blk; k += ctas) {
-            const int n = k / p.rb2, rb = k % p.rb2;
+        UnitWalk uw(cta_in, ctas, p.rb2);
+        for (int k = cta_in; k < p.units_blk; k += ctas, uw.next()) {
+            const int n = uw.n, rb = uw.rb;
             ptx::mbar_wait(empty_bar(b), ph ^ 1);
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(full_bar(b), halo_bytes);
@@ -595,8 +612,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         int acc = 0;
         uint32_t aph = 0;
         int ui = 0;
-        for (int k = cta_in; k < p.units_blk; k += ctas, ++ui) {
-            const int n = k / p.rb2, oh0 = (k % p.rb2) * R2, oh = oh0 + r;
+        UnitWalk uw(cta_in, ctas, p.rb2);
+        for (int k = cta_in; k < p.units_blk; k += ctas, ++ui, uw.next()) {
+            const int n = uw.n, oh0 = uw.rb * R2, oh = oh0 + r;
             const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
             const uint32_t stg = stg0 + (uint32_t)((ui & 1) * 1024);
             // the store issued from this buffer two units ago has read it
