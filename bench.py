@@ -158,6 +158,8 @@ def max_over_ranks(vals, device, world):
         return [float(v) for v in vals]
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":  # shared-GPU smoke mode (Q8G_BENCH_SHARED_GPU): host tensors
+        device = "cpu"
     t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(v) for v in t.cpu()]
@@ -625,13 +627,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Q8G_BENCH_SHARED_GPU=1 (tests only, never a measurement): every rank on
+    # cuda:0 with a gloo group, to exercise the N > 1 code path on a one-GPU box
+    shared = world > 1 and os.environ.get("Q8G_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if (world == 1 or shared) else local
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(gpu)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", gpu)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     ctx = {"dev": dev, "rank": rank, "world": world, "stream": stream, "lib": _lib.load()}

@@ -83,3 +83,32 @@ def test_our_arm_line_on_the_gpu(cfg):
     sys.path.insert(0, str(ROOT))
     import bench
     assert d["config"] == bench.config_dict(cfg, 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
+def test_multirank_bench_path_on_one_gpu(cfg):
+    """The N > 1 code path of bench.py (torchrun, 2 ranks, strong scaling:
+    C2 row stripes, C3 / C4 image ranges, max-over-ranks timing) run with both
+    ranks sharing cuda:0 over gloo (Q8G_BENCH_SHARED_GPU=1).  A smoke test of
+    the launch, partition and reduction plumbing that the driver's scaling run
+    uses -- the numbers of a shared GPU are not measurements."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, Q8G_BENCH_SHARED_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--gpus",
+                        "2", "--config", cfg, "--steps", "2", "--warmup", "3", "--no-sub", "--no-cpu-baseline"],
+                       capture_output=True, text=True, cwd=ROOT, env=env, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    d = json.loads(lines[0])
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert d["n_gpus"] == 2 and d["config"] == bench.config_dict(cfg, 2) and d["scaling"] == "strong"
+    assert d["value"] > 0 and d["gpu_launches"] == 2 and d["e2e"]["value"] > 0
+    per_gpu = bench.int8_peaks()[0] if cfg == "C2" else bench.peaks()[0]
+    assert d["roofline"]["peak"] == pytest.approx(2 * per_gpu)
