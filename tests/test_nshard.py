@@ -209,3 +209,41 @@ def test_gemm_to_peers_argument_errors(cuda):
     rc = lib.q8g_gemm_u8s8_requant_peers(a.data_ptr(), 16, 32, 32, pw.handle, pipe.epilogue(pw), out.data_ptr(),
                                          plist, 1, 64, 0, 16, None, None)
     assert rc == q8._lib.Q8G_EINVAL and b"device memory" in lib.q8g_last_error()
+
+
+def _nccl_one_rank(mode, q):
+    """world 1 over NCCL on cuda:0: the symmetric-memory allocation,
+    rendezvous and barrier of "peers" mode, or the NCCL all-gather of
+    "allgather" mode, around the device GEMM."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(_free_port())
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        import paper_2101_05615_b200 as q8
+        m, n, k = 2048, 1024, 256
+        orc, a, b, bias, zp_b, mult = _problem(m, n, k, seed=5)
+        g = q8.NShardedGemm(b, _rp(q8, k, bias, zp_b, mult), relu=True, m_max=m, mode=mode)
+        out = g(torch.from_numpy(a).cuda())
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        want = _expected(orc, a, b, bias, zp_b, mult)
+        q.put((g.mode, bool((got == want).all())))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put(("error", traceback.format_exc()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["peers", "allgather"])
+def test_nsharded_gemm_nccl_world_one(cuda, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_one_rank, args=(mode, q))
+    p.start()
+    got_mode, ok = q.get(timeout=300)
+    p.join(timeout=60)
+    assert got_mode == mode, ok
+    assert ok is True
