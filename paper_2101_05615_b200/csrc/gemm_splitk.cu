@@ -125,16 +125,7 @@ __device__ __forceinline__ void cluster_arrive_release() {
 __device__ __forceinline__ void cluster_wait_acquire() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// L2-only 16-byte global store / load (split-K exchange workspace)
-__device__ __forceinline__ void st_cg_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.global.cg.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
-    uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-    return v;
-}
-// 32-byte (256-bit) variants: half the L2 requests of v4; measured ~2x the
+// L2-only 32-byte (256-bit) global stores / loads (split-K exchange workspace): half the L2 requests of v4; measured ~2x the
 // per-SM read bandwidth from L2 (tools/l2_bw.cu)
 __device__ __forceinline__ void st_cg_v8(void* p, const uint32_t* v) {
     asm volatile("st.global.cg.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
@@ -161,6 +152,85 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
     uint32_t d;
     asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
+}
+
+
+// requant (MODE 1 / 2) or raw int32 (MODE 0) + store of one row's 16 owned
+// columns [col0, col0 + 16) (row < rows, col0 < n checked by the caller)
+template <int MODE>
+__device__ __forceinline__ void sk_store16(const SkParams& p, const int4* rec16, uint32_t (&v)[16], int32_t rowsum,
+                                           int row, int col0) {
+    if (MODE == 0) {
+        int32_t* dst = reinterpret_cast<int32_t*>(p.c) + (size_t)row * p.ldc + col0;
+        int32_t out[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            int32_t x = (int32_t)v[j];
+            if (p.bias_add && col0 + j < p.n)
+                x = (int32_t)((uint32_t)x + (uint32_t)__ldg(p.bias_add + col0 + j));
+            out[j] = x;
+        }
+        const bool vec = (col0 + 16 <= p.n) && ((p.ldc & 3) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+        if (vec) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<int4*>(dst + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
+        } else {
+            for (int j = 0; j < 16; ++j)
+                if (col0 + j < p.n) dst[j] = out[j];
+        }
+        return;
+    }
+    uint32_t packed[4];
+    if (MODE == 1 && p.fast) {
+        // F32_RNE, 0 <= zp_c <= 255, finite multipliers: magic-add
+        // rounding + saturating pack (exact; see conv_tc.cu epi_f32_fast)
+        const int32_t zoff = 0x4B400000 - p.zp_c;
+        const float floor_x = p.relu ? 0.0f : -8388608.0f;
+        const uint32_t nrowsum = 0u - (uint32_t)rowsum;  // once per row, not per value
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            int32_t rr[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = w * 4 + b;
+                const int4 r4 = rec16[j];
+                const int32_t adj = (int32_t)(v[j] + ((uint32_t)r4.x + (uint32_t)r4.y * nrowsum));
+                float x = __fmul_rn(__int2float_rn(adj), __int_as_float(r4.z));
+                x = fmaxf(x, floor_x);
+                rr[b] = __float_as_int(__fadd_rn(x, 12582912.0f)) - zoff;
+            }
+            packed[w] = pack_sat_u8(rr[1], rr[0], pack_sat_u8(rr[3], rr[2], 0u));
+        }
+    } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = w * 4 + b;
+                const int4 r4 = rec16[j];
+                EpiRecord rc;
+                rc.c = r4.x;
+                rc.zpb = r4.y;
+                const int32_t adj = adjust((int32_t)v[j], rowsum, rc);
+                const uint32_t q = MODE == 1 ? requant_f32(adj, __int_as_float(r4.z), p.zp_c, p.relu)
+                                             : requant_ref(adj, __hiloint2double(r4.w, r4.z), p.zp_c, p.relu);
+                word |= q << (8 * b);
+            }
+            packed[w] = word;
+        }
+    }
+    uint8_t* dst = reinterpret_cast<uint8_t*>(p.c) + (size_t)row * p.ldc + col0;
+    const bool vec = (col0 + 16 <= p.n) && ((p.ldc & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+    if (vec) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    } else {
+        for (int j = 0; j < 16; ++j)
+            if (col0 + j < p.n) dst[j] = (uint8_t)(packed[j / 4] >> (8 * (j % 4)));
+    }
 }
 
 template <int BN, int S, int AST, int BST, int MODE, bool RS>
@@ -397,77 +467,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
                 for (int j = 0; j < 16; ++j) v[j] += rx[hh][sl][j];
             const int col0 = n0 + (int)rank * OWN + h * 16;
             if (row >= p.rows || col0 >= p.n) continue;
-            if (MODE == 0) {
-                int32_t* dst = reinterpret_cast<int32_t*>(p.c) + (size_t)row * p.ldc + col0;
-                int32_t out[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    int32_t x = (int32_t)v[j];
-                    if (p.bias_add && col0 + j < p.n)
-                        x = (int32_t)((uint32_t)x + (uint32_t)__ldg(p.bias_add + col0 + j));
-                    out[j] = x;
-                }
-                const bool vec = (col0 + 16 <= p.n) && ((p.ldc & 3) == 0) &&
-                                 ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-                if (vec) {
-#pragma unroll
-                    for (int j = 0; j < 16; j += 4)
-                        *reinterpret_cast<int4*>(dst + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
-                } else {
-                    for (int j = 0; j < 16; ++j)
-                        if (col0 + j < p.n) dst[j] = out[j];
-                }
-                continue;
-            }
-            uint32_t packed[4];
-            if (MODE == 1 && p.fast) {
-                // F32_RNE, 0 <= zp_c <= 255, finite multipliers: magic-add
-                // rounding + saturating pack (exact; see conv_tc.cu epi_f32_fast)
-                const int32_t zoff = 0x4B400000 - p.zp_c;
-                const float floor_x = p.relu ? 0.0f : -8388608.0f;
-                const uint32_t nrowsum = 0u - (uint32_t)rowsum;  // once per row, not per value
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    int32_t rr[4];
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int j = w * 4 + b;
-                        const int4 r4 = recs[h * 16 + j];
-                        const int32_t adj = (int32_t)(v[j] + ((uint32_t)r4.x + (uint32_t)r4.y * nrowsum));
-                        float x = __fmul_rn(__int2float_rn(adj), __int_as_float(r4.z));
-                        x = fmaxf(x, floor_x);
-                        rr[b] = __float_as_int(__fadd_rn(x, 12582912.0f)) - zoff;
-                    }
-                    packed[w] = pack_sat_u8(rr[1], rr[0], pack_sat_u8(rr[3], rr[2], 0u));
-                }
-            } else {
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    uint32_t word = 0;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int j = w * 4 + b;
-                        const int4 r4 = recs[h * 16 + j];
-                        EpiRecord rc;
-                        rc.c = r4.x;
-                        rc.zpb = r4.y;
-                        const int32_t adj = adjust((int32_t)v[j], rowsum, rc);
-                        const uint32_t q = MODE == 1 ? requant_f32(adj, __int_as_float(r4.z), p.zp_c, p.relu)
-                                                     : requant_ref(adj, __hiloint2double(r4.w, r4.z), p.zp_c, p.relu);
-                        word |= q << (8 * b);
-                    }
-                    packed[w] = word;
-                }
-            }
-            uint8_t* dst = reinterpret_cast<uint8_t*>(p.c) + (size_t)row * p.ldc + col0;
-            const bool vec = (col0 + 16 <= p.n) && ((p.ldc & 15) == 0) &&
-                             ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-            if (vec) {
-                *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            } else {
-                for (int j = 0; j < 16; ++j)
-                    if (col0 + j < p.n) dst[j] = (uint8_t)(packed[j / 4] >> (8 * (j % 4)));
-            }
+            sk_store16<MODE>(p, recs + h * 16, v, rowsum, row, col0);
         }
         if (warp == 4 && lane == 0) sk_stamp(p, 7);
     } else {
