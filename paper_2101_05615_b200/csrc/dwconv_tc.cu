@@ -549,9 +549,18 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas) {
+            const long long ck0 = clock64();
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
+            const long long ck1 = clock64();
             ptx::mbar_wait(full_bar(b), ph);
             ptx::tc_fence_after();
+            const long long ck2 = clock64();
+            if (lane == 0 && p.trace && blockIdx.x == 0 && (k - cta_in) / ctas < 64) {
+                const int u = (k - cta_in) / ctas;
+                p.trace[8192 + 24 * 64 + u] = (unsigned long long)(ck1 - ck0);
+                p.trace[8192 + 25 * 64 + u] = (unsigned long long)(ck2 - ck1);
+                p.trace[8192 + 26 * 64 + u] = (unsigned long long)ck0;
+            }
             const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride) >> 4);  // TMEM lane m = output column m
             if (ptx::elect_one()) {
                 dw_stamp(p, 1, (k - cta_in) / ctas);
@@ -591,6 +600,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             if (++acc == 2) {
                 acc = 0;
                 aph ^= 1;
+            }
+        }
+    } else if (warp == EPI64 + 2 && p.trace) {
+        // debug trace only: the time each halo actually lands (the MMA warp's
+        // own stamp also includes its wait for a free accumulator)
+        int b = 0;
+        uint32_t ph = 0;
+        for (int k = cta_in; k < p.units_blk; k += ctas) {
+            ptx::mbar_wait(full_bar(b), ph);
+            if (lane == 0) dw_stamp(p, 5, (k - cta_in) / ctas);
+            if (++b == p.nb2) {
+                b = 0;
+                ph ^= 1;
             }
         }
     } else if (warp < EPI64) {
@@ -635,7 +657,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+            if (lane == 0) {
+                ptx::mbar_arrive(tempty_bar(acc));
+                dw_stamp(p, 7 + ew, ui);  // debug trace: this warp released the accumulator
+            }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {  // 16 channels at a time
                 const int4* cq = reinterpret_cast<const int4*>(corr_s + cls * CB + j * 32 + hh * 16);
