@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <fstream>
 #include <cstring>
+#include <array>
 #include <functional>
 #include <string>
 #include <thread>
@@ -259,6 +260,82 @@ bool criterion6(std::string& d) {
     return true;
 }
 
+// ---- criterion 9 (N-sharded multi-GPU): every rank of a
+// column split, run on this one GPU with its own output buffer standing in
+// for a peer's, writes its shard into all buffers through
+// execute_gemm_to_peers; each buffer must equal the unsharded GEMM ----
+bool criterion9(std::string& d) {
+    Rng rng(9009);
+    for (const auto& shape : std::vector<std::array<int, 4>>{{4864, 2048, 256, 2}, {128, 1024, 512, 3}}) {
+        const int m = shape[0], n = shape[1], k = shape[2], world = shape[3];
+        const auto a = rng.u8(m, k);
+        const auto b = rng.i8(k, n);
+        RequantParams rp;
+        rp.zp_a = 128;
+        rp.zp_c = 5;
+        rp.k_total = k;
+        rp.rounding = Rounding::kF32Rne;
+        for (int j = 0; j < n; ++j) {
+            rp.bias.push_back(rng.integer(-1000, 1000));
+            rp.zp_b_per_channel.push_back(rng.integer(-10, 10));
+            rp.multiplier_f32_per_channel.push_back(0.0005f + 0.0015f * (float)rng.integer(0, 1000) / 1000.0f);
+        }
+        uint8_t* da = nullptr;
+        cudaMalloc(&da, (size_t)m * k);
+        cudaMemcpy(da, a.data(), (size_t)m * k, cudaMemcpyHostToDevice);
+        // unsharded
+        const PackedWeight pw = prepack_weights(cview(b), BlockingParams::defaults());
+        const OutputPipeline whole({ReluQuantized{}, Requantize{rp, nullptr}});
+        uint8_t* dref = nullptr;
+        cudaMalloc(&dref, (size_t)m * n);
+        execute_gemm(DeviceView<const uint8_t>{da, m, k, k}, pw, DeviceView<uint8_t>{dref, m, n, n}, whole,
+                     KernelVariant::kAccI32, 0, 1);
+        std::vector<uint8_t> ref((size_t)m * n);
+        cudaMemcpy(ref.data(), dref, ref.size(), cudaMemcpyDeviceToHost);
+        // sharded: columns [n0, n1) per rank, 16-column blocks (nshard.column_shard)
+        std::vector<uint8_t*> bufs(world);
+        for (auto& p : bufs) {
+            cudaMalloc(&p, (size_t)m * n);
+            cudaMemset(p, 0xA5, (size_t)m * n);
+        }
+        const int blocks = (n + 15) / 16;
+        for (int r = 0; r < world; ++r) {
+            int b0 = 0, b1 = 0;
+            q8g_partition_stripes(blocks, r, world, &b0, &b1);
+            const int n0 = std::min(16 * b0, n), n1 = std::min(16 * b1, n);
+            if (n1 <= n0) continue;
+            Matrix<int8_t> bs(k, n1 - n0);
+            for (int kk = 0; kk < k; ++kk)
+                for (int j = n0; j < n1; ++j) bs(kk, j - n0) = b(kk, j);
+            RequantParams rs = rp;
+            rs.bias.assign(rp.bias.begin() + n0, rp.bias.begin() + n1);
+            rs.zp_b_per_channel.assign(rp.zp_b_per_channel.begin() + n0, rp.zp_b_per_channel.begin() + n1);
+            rs.multiplier_f32_per_channel.assign(rp.multiplier_f32_per_channel.begin() + n0,
+                                                 rp.multiplier_f32_per_channel.begin() + n1);
+            const PackedWeight pws = prepack_weights(cview(bs), BlockingParams::defaults());
+            const OutputPipeline shard({ReluQuantized{}, Requantize{rs, nullptr}});
+            std::vector<uint8_t*> peers;
+            for (int q = 0; q < world; ++q)
+                if (q != r) peers.push_back(bufs[q]);
+            execute_gemm_to_peers(DeviceView<const uint8_t>{da, m, k, k}, pws, DeviceView<uint8_t>{bufs[r], m, n, n},
+                                  peers, n0, shard);
+        }
+        cudaDeviceSynchronize();
+        bool ok = true;
+        for (auto* p : bufs) {
+            std::vector<uint8_t> h((size_t)m * n);
+            cudaMemcpy(h.data(), p, h.size(), cudaMemcpyDeviceToHost);
+            ok = ok && h == ref;
+            cudaFree(p);
+        }
+        cudaFree(da);
+        cudaFree(dref);
+        if (!ok) return d = "sharded != unsharded at m=" + std::to_string(m), false;
+    }
+    d = "column shards written to every rank's output equal the unsharded GEMM (2 and 3 ranks)";
+    return true;
+}
+
 // ---- criterion 3: outlier split + SpMDMAdd reproduce the unsplit GEMM; WriteDequantF32 ----
 bool criterion3(std::string& d) {
     Rng rng(3003);
@@ -422,6 +499,7 @@ int main(int argc, char** argv) {
         run(6, criterion6);
         run(7, criterion7);
         run(8, criterion8);
+        run(9, criterion9);
         if (!cli_path.empty()) run(8, criterion8_cli);
     }
     if (failures == 0) {

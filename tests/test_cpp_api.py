@@ -32,4 +32,4 @@ def test_cpp_acceptance_on_gpu(runner, cuda):
     r = subprocess.run([str(runner), "gpu", str(cli)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("[PASS]") == 9  # 0 host + 1, 2, 3 (outliers), 5, 6, 7, 8, 8 (CLI leg)
+    assert r.stdout.count("[PASS]") == 10  # 0 host + 1, 2, 3 (outliers), 5, 6, 7, 8, 8 (CLI leg), 9 (N-sharded)
