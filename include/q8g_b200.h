@@ -142,7 +142,8 @@ int q8g_gemm_u8s8_requant(const uint8_t* a_dev, int m, int k, int lda, const q8g
  * The CTA-pair kernel stores each tile to the peers straight from its
  * staging tile (TMA stores over NVLink, overlapped with the GEMM); other
  * kernels copy the finished stripe with the copy engines.  Peer access is
- * enabled on first use.  Completion on the peers is ordered by `stream`:
+ * enabled on first use; between devices with no P2P path every peer gets a
+ * staged copy instead.  Completion on the peers is ordered by `stream`:
  * the caller synchronises the ranks (e.g. a barrier after a stream sync)
  * before reading the gathered output. */
 int q8g_gemm_u8s8_requant_peers(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,

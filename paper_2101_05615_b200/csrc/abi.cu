@@ -523,7 +523,7 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
                        const q8g_epilogue* ep, const int32_t* bias_add, void* c, int ldc,
                        int row_begin, int row_end, q8g_kernel_cache* cache, cudaStream_t s,
                        bool raw, const uint32_t* a_ready = nullptr, uint32_t a_epoch = 0,
-                       uint8_t* const* c_peers = nullptr, int n_peers = 0) {
+                       uint8_t* const* c_peers = nullptr, int n_peers = 0, bool peers_direct = true) {
     if (!pb) return fail(Q8G_EINVAL, "execute_gemm: null packed weight");
     if (k != pb->k) return fail(Q8G_EINVAL, "execute_gemm: A columns must equal the packed weight K");
     if (m < 1 || lda < k || ldc < pb->n || !a || !c)
@@ -554,8 +554,8 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
     uint8_t* peers[kMaxPeers];
     bool peers_written = false;
     for (int d = 0; d < n_peers; ++d) peers[d] = c_peers[d] + (size_t)row_begin * ldc;
-    g.c_peers = peers;
-    g.n_peers = n_peers;
+    g.c_peers = peers_direct ? peers : nullptr;  // kernels store to the peers only over P2P
+    g.n_peers = peers_direct ? n_peers : 0;
     g.peers_written = &peers_written;
     const int kind = resolve_tile(cache ? cache : &process_cache(), g.rows, pb->n, k,
                                   a_is_tma_aligned(g.a, lda));
@@ -579,21 +579,30 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
 }
 
 // peer access from `dev` to the device holding `ptr` (once per pair);
-// Q8G_OK also when ptr is on `dev` itself
-static int enable_peer_access(int dev, const void* ptr) {
+// Q8G_OK also when ptr is on `dev` itself.  *direct = false when the devices
+// have no P2P path: the stripe then reaches that peer by a staged copy.
+static int enable_peer_access(int dev, const void* ptr, bool* direct) {
     cudaPointerAttributes at{};
     cudaError_t e = cudaPointerGetAttributes(&at, ptr);
     if (e != cudaSuccess) return cuda_fail(e, "gemm_peers: cudaPointerGetAttributes");
     if (at.type != cudaMemoryTypeDevice) return fail(Q8G_EINVAL, "gemm_peers: peer output must be device memory");
     if (at.device == dev) return Q8G_OK;
     static std::mutex mu;
-    static std::set<std::pair<int, int>> done;
+    static std::set<std::pair<int, int>> done, no_p2p;
     std::lock_guard<std::mutex> lock(mu);
     if (done.count({dev, at.device})) return Q8G_OK;
+    if (no_p2p.count({dev, at.device})) {
+        *direct = false;
+        return Q8G_OK;
+    }
     int can = 0;
     e = cudaDeviceCanAccessPeer(&can, dev, at.device);
     if (e != cudaSuccess) return cuda_fail(e, "gemm_peers: cudaDeviceCanAccessPeer");
-    if (!can) return fail(Q8G_ENOTSUP, "gemm_peers: no peer access between the devices");
+    if (!can) {
+        no_p2p.insert({dev, at.device});
+        *direct = false;
+        return Q8G_OK;
+    }
     DeviceGuard dg(dev);
     e = cudaDeviceEnablePeerAccess(at.device, 0);
     if (e == cudaErrorPeerAccessAlreadyEnabled) {
@@ -618,15 +627,16 @@ int q8g_gemm_u8s8_requant_peers(const uint8_t* a_dev, int m, int k, int lda, con
                                 void* stream) {
     if (n_peers < 0 || n_peers > kMaxPeers) return fail(Q8G_EINVAL, "gemm_peers: 0 to 7 peer outputs");
     if (n_peers > 0 && !c_peer_dev) return fail(Q8G_EINVAL, "gemm_peers: null peer output list");
+    bool direct = true;
     for (int d = 0; d < n_peers; ++d) {
         if (!c_peer_dev[d]) return fail(Q8G_EINVAL, "gemm_peers: null peer output");
         if (pb) {
-            const int st = enable_peer_access(pb->device, c_peer_dev[d]);
+            const int st = enable_peer_access(pb->device, c_peer_dev[d], &direct);
             if (st != Q8G_OK) return st;
         }
     }
     return gemm_common(a_dev, m, k, lda, pb, ep, nullptr, c_dev, ldc, row_begin, row_end, cache,
-                       (cudaStream_t)stream, false, nullptr, 0, c_peer_dev, n_peers);
+                       (cudaStream_t)stream, false, nullptr, 0, c_peer_dev, n_peers, direct);
 }
 
 int q8g_gemm_u8s8_raw_i32(const uint8_t* a_dev, int m, int k, int lda, const q8g_packed_b* pb,
