@@ -170,7 +170,13 @@ class NShardedGemm:
             if self.pw is not None:
                 # the peers' outputs share this buffer's leading dimension (n)
                 execute_gemm_to_peers(a, self.pw, out, self.peer_ptrs, self.pipeline, self.n0, stream=stream)
-            self.handle.barrier()  # every rank's peer stores have landed
+            # every rank's peer stores have landed: the symmetric-memory barrier
+            # runs on the GEMM's stream, after this rank's stores
+            if stream is None:
+                self.handle.barrier()
+            else:
+                with torch.cuda.stream(stream):
+                    self.handle.barrier()
             return out
         wmax = max(self.widths)
         shard = torch.zeros((m, wmax), dtype=torch.uint8, device=self.device)
