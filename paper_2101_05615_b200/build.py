@@ -16,7 +16,11 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
+# Q8G_CHECKED=1: the checked library (device-side bounds / layout assertions,
+# Q8G_CHECK in ptx.cuh) from its own object directory, linked to the same
+# libq8g_b200.so name so the package and the tests load it unchanged
+CHECKED = os.environ.get("Q8G_CHECKED") == "1"
+BUILD = PKG / ("_build_checked" if CHECKED else "_build")
 LIB = PKG / "libq8g_b200.so"
 ROOT = PKG.parent
 
@@ -27,7 +31,7 @@ NVFLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
     "-Xptxas", "-warn-spills",
     f"-I{ROOT / 'include'}",
-]
+] + (["-DQ8G_CHECKED=1"] if CHECKED else [])
 
 
 def _sources():
@@ -61,7 +65,9 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     newest = max(o.stat().st_mtime for o in objs)
-    if LIB.exists() and LIB.stat().st_mtime >= newest:
+    stamp = BUILD / "linked"  # which object set the current library was linked from
+    if LIB.exists() and LIB.stat().st_mtime >= newest and stamp.exists() and \
+            stamp.read_text() == str(LIB.stat().st_mtime_ns):
         return LIB
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
            "-lcuda" if False else "-ldl"]
@@ -70,6 +76,9 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    for d in {PKG / "_build", PKG / "_build_checked"} - {BUILD}:  # the other object set is stale now
+        (d / "linked").unlink(missing_ok=True)
+    stamp.write_text(str(LIB.stat().st_mtime_ns))
     return LIB
 
 

@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
     const CvLayout L = cv_layout(p);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)L.total <= ptx::dynamic_smem_size());
     // roles: warps 0..EPI_WARPS-1 epilogue (TMEM lane quarter = warp % 4), then
     // the halo producer, MMA issuer 0 (SMSP 1), the TMEM allocator and MMA
     // issuer 1 (SMSP 3): the scheduler favours the highest warp id, so the
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
             const bool valid = orow < ROWS && oh < p.h && ocol >= 0 && ocol < p.w;
             const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
             const size_t pix = ((size_t)n * p.h + oh) * p.w + ocol;
+            Q8G_CHECK(u < p.units && (!valid || pix < (size_t)p.nb * p.h * p.w));
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
             if (quarter == 0 && lane == 0) cv_stamp(p, 3, i);

@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     dwconv_fma_kernel(const __grid_constant__ CUtensorMap tmap_x, const DwfParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)SMEM <= ptx::dynamic_smem_size());
     const uint32_t base = ptx::smem_u32(smem);
     float4* consts = reinterpret_cast<float4*>(smem + NST * STAGE);  // [32 lanes][binit, mscale]
     Ctx c{p};

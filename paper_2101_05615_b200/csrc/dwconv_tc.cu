@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
     const DwLayout L = dw_layout(p.halo_bytes, p.groups);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)L.total <= ptx::dynamic_smem_size());
     const uint32_t bar0 = base + L.bar_off;
     auto full_bar = [&](int b) { return bar0 + 8u * b; };
     auto empty_bar = [&](int b) { return bar0 + 8u * (NBUF + b); };
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
     const Dw2Layout L = dw2_layout(p.wp, p.nb2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)L.total <= ptx::dynamic_smem_size() && p.nb2 >= 2 && p.nb2 <= NB2);
     const uint32_t bar0 = base + L.bar_off;
     auto full_bar = [&](int b) { return bar0 + 8u * b; };
     auto empty_bar = [&](int b) { return bar0 + 8u * (NB2 + b); };
@@ -637,6 +639,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         UnitWalk uw(cta_in, ctas, p.rb2);
         for (int k = cta_in; k < p.units_blk; k += ctas, ++ui, uw.next()) {
             const int n = uw.n, oh0 = uw.rb * R2, oh = oh0 + r;
+            Q8G_CHECK(n >= 0 && n < p.nb && oh0 < p.h && uw.rb < p.rb2);
             const int cls = (oh == 0 ? 1 : 0) | (oh == p.h - 1 ? 2 : 0) | (ocol == 0 ? 4 : 0) | (ocol == p.w - 1 ? 8 : 0);
             const uint32_t stg = stg0 + (uint32_t)((ui & 1) * 1024);
             // the store issued from this buffer two units ago has read it

@@ -80,6 +80,7 @@ struct SkParams {
     // L2 exchange workspace [tile][owner][S-1 slots] of SLOT_BYTES; null =
     // push the slots into the owners' smem (DSMEM)
     uint8_t* ws;
+    size_t ws_bytes;  // its size (checked builds assert every slot access is inside it)
     // host-view overlap: A lands by a concurrent copy that then writes a_epoch
     // to *a_ready (GemmArgs); null = A resident
     const uint32_t* a_ready;
@@ -160,6 +161,7 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t a, int32_t b, uint32_t c
 template <int MODE>
 __device__ __forceinline__ void sk_store16(const SkParams& p, const int4* rec16, uint32_t (&v)[16], int32_t rowsum,
                                            int row, int col0) {
+    Q8G_CHECK(row >= 0 && row < p.rows && col0 >= 0 && col0 < p.n);
     if (MODE == 0) {
         int32_t* dst = reinterpret_cast<int32_t*>(p.c) + (size_t)row * p.ldc + col0;
         int32_t out[16];
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)Cfg::SMEM_BYTES <= ptx::dynamic_smem_size());
     ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) sk_stamp(p, 0);
     const uint32_t rank = ptx::cluster_ctarank();
@@ -420,6 +423,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
             const int q = ((int)rank + 1 + qi) % S;
             const int dslot = ((int)rank - q + S) % S - 1;  // at owner q: slot of this source
             uint8_t* slot = p.ws + ((size_t)(tile * S + q) * (S - 1) + dslot) * Cfg::SLOT_BYTES;
+            Q8G_CHECK(dslot >= 0 && dslot < S - 1 && slot + Cfg::SLOT_BYTES <= p.ws + p.ws_bytes);
 #pragma unroll
             for (int h = g; h < NH; h += 2) {
                 uint32_t v[16];
@@ -440,6 +444,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
         // ---- reduce the owned columns: own partial + the S-1 received slots,
         // all loads in flight at once (one L2 round trip)
         const uint8_t* recv = p.ws + (size_t)(tile * S + (int)rank) * (S - 1) * Cfg::SLOT_BYTES;
+        Q8G_CHECK(recv + (S - 1) * Cfg::SLOT_BYTES <= p.ws + p.ws_bytes);
         const int row = m0 + r;
         int32_t rowsum = my_rs;
         if (RS) {
@@ -549,7 +554,8 @@ cudaError_t launch_sk(const GemmArgs& g, cudaStream_t s) {
         static int parity = 0;
         p.trace_cta = p.trace + (parity ^= 1) * 4096;
     }
-    p.ws = splitk_workspace(dev, s, (size_t)tiles * S * (S - 1) * Cfg::SLOT_BYTES);
+    p.ws_bytes = (size_t)tiles * S * (S - 1) * Cfg::SLOT_BYTES;
+    p.ws = splitk_workspace(dev, s, p.ws_bytes);
     if (!p.ws) return cudaErrorNotSupported;  // caller falls back to the non-split kernel
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tiles * S);

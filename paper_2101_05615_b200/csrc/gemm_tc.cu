@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(RS ? 384 : 256, 1)
     uint8_t* smem = smem_raw + (base - raw_addr);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)Cfg::SMEM_BYTES <= ptx::dynamic_smem_size());
     ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) trace_stamp(p, 0);
     const uint32_t rank = CN > 1 ? ptx::cluster_ctarank() : 0;

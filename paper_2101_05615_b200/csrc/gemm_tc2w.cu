@@ -278,6 +278,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t base = (raw_addr + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base - raw_addr);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    Q8G_CHECK((uint32_t)Cfg::SMEM_BYTES <= ptx::dynamic_smem_size());
+    Q8G_CHECK(p.n_peers >= 0 && p.n_peers <= kMaxPeers);
     ptx::griddep_launch_dependents();
     if (threadIdx.x == 0) tw_clk(p, 0);
     const uint32_t rank = ptx::cluster_ctarank();  // 0 leader, 1 follower

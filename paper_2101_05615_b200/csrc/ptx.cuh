@@ -8,8 +8,32 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 namespace q8g {
 namespace ptx {
+
+// Checked builds (Q8G_CHECKED=1 python -c "...build()"): device-side bounds
+// and layout assertions that trap on failure -- this pool refuses
+// compute-sanitizer, so the GPU suite runs against a checked library instead.
+#ifdef Q8G_CHECKED
+#define Q8G_CHECK(cond)                                                                                   \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("Q8G_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,       \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                    \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define Q8G_CHECK(cond) ((void)0)
+#endif
+// dynamic shared memory of the launch, in bytes
+__device__ __forceinline__ uint32_t dynamic_smem_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
