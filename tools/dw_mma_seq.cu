@@ -9,7 +9,8 @@
 //   2  the kernel's sequence with every N = 128 MMA replaced by N = 64;
 //   3  variant 0 + 16 warps reading TMEM (the epilogue's tcgen05.ld traffic);
 //   4  variant 0 + 16 warps storing / loading shared memory (STS.128 + LDS.128);
-//   5  variant 0 + 16 warps of FP / integer ALU work (the requant arithmetic).
+//   5  variant 0 + 16 warps of FP / integer ALU work (the requant arithmetic);
+//   6  variant 0 with A rotating over 3 halo buffers at the kernel's stride.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_2101_05615_b200/csrc dw_mma_seq.cu -o dw_mma_seq
 #include <cstdio>
@@ -33,7 +34,9 @@ __global__ void __launch_bounds__(544, 1) seq(int variant, int units, unsigned l
     __shared__ uint32_t tmem_slot;
     const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     const int wp = 114, CB = 64, KG = 2;
-    const uint32_t sA = base, sB = base + 4 * wp * CB + 2048 + 1024;  // halo (4 rows) + guard, then B
+    // halo buffers (4 rows + guard, the kernel's stride) then B
+    const uint32_t hstride = (uint32_t)((4 * wp * CB + 1024 + 1023) / 1024 * 1024);
+    const uint32_t sA = base + 1024, sB = sA + 3 * hstride;
     if (threadIdx.x == 0) {
         ptx::mbar_init(ptx::smem_u32(&bar), 1);
         ptx::fence_mbar_init();
@@ -60,12 +63,12 @@ __global__ void __launch_bounds__(544, 1) seq(int variant, int units, unsigned l
 #pragma unroll
                 for (int c = 0; c < 4; ++c) sink += v[c][0] + v[c][15];
             } else if (variant == 4) {
-                const uint32_t a = base + 64 * 1024 + (uint32_t)((w * 32 + threadIdx.x % 32) * 16);
+                const uint32_t a = base + 140 * 1024 + (uint32_t)((w * 32 + threadIdx.x % 32) * 16);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(sink) : "memory");
                     uint4 x;
-                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(base + 70000u) : "memory");
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(base + 190000u) : "memory");
                     sink += x.x;
                 }
             } else if (variant == 5) {
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(544, 1) seq(int variant, int units, unsigned l
     constexpr uint32_t idesc64 = ptx::idesc_u8s8_s32<128, 64>();
     constexpr uint32_t idesc128 = ptx::idesc_u8s8_s32<128, 128>();
     const uint64_t a0 = swz64_desc(sA);
+    const uint64_t hstride16 = hstride >> 4;
     const uint64_t row16 = (uint64_t)(wp * CB / 16), pos16 = CB / 16;
     const uint64_t b0 = noswz_desc(sB, 192 * 16, 128);
     const uint32_t bar_a = ptx::smem_u32(&bar);
@@ -102,7 +106,8 @@ __global__ void __launch_bounds__(544, 1) seq(int variant, int units, unsigned l
 #pragma unroll
                     for (int j = 0; j < KG; ++j) {
                         const int i = (ii + 3) % 4;
-                        const uint64_t ad = a0 + (uint64_t)i * row16 + (uint64_t)kw * pos16 + 2u * j;
+                        const uint64_t ad = a0 + (variant == 6 ? (uint64_t)(u % 3) * hstride16 : 0) +
+                                            (uint64_t)i * row16 + (uint64_t)kw * pos16 + 2u * j;
                         const uint64_t bd = b0 + (uint64_t)((kw * KG + j) * 384);
                         uint32_t d = tmem + (uint32_t)(acc * 256 + j * 128);
                         if (variant == 1) d = tmem + (uint32_t)((region++ % 4) * 128);
@@ -132,14 +137,14 @@ __global__ void __launch_bounds__(544, 1) seq(int variant, int units, unsigned l
 
 int main() {
     setvbuf(stdout, nullptr, _IONBF, 0);
-    const int units = 200, smem = 120 * 1024;  // halo + B below 64 KB; STS at 64 KB
+    const int units = 200, smem = 200 * 1024;  // 3 halos + B below 130 KB; STS at 64 KB (variant 4 only)
     unsigned long long* d_out;
     cudaMalloc(&d_out, 148 * sizeof(unsigned long long));
     cudaFuncSetAttribute(seq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"kernel sequence", "own D region per MMA", "all N = 64", "+ TMEM readers",
-                           "+ shared-memory STS/LDS", "+ ALU warps"};
+                           "+ shared-memory STS/LDS", "+ ALU warps", "A over 3 halo buffers"};
     cudaMalloc(&d_out, 1024 * sizeof(unsigned long long));
-    for (int v = 0; v < 6; ++v) {
+    for (int v = 0; v < 7; ++v) {
         seq<<<148, 544, smem>>>(v, units, d_out);
         seq<<<148, 544, smem>>>(v, units, d_out);
         cudaError_t e = cudaDeviceSynchronize();
