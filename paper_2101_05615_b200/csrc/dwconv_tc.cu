@@ -533,7 +533,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 ptx::mbar_arrive_expect_tx(full_bar(b), halo_bytes);
                 // box {64 ch, W+2 px, R2+2 rows, 1} at (c0, col -1, row rb*R2-1, image n)
                 tma_load_4d(base + L.halo_off + b * L.halo_stride, &tmap_x, c0, -1, rb * R2 - 1, n, full_bar(b));
+#ifdef Q8G_DW_TRACE
                 dw_stamp(p, 0, (k - cta_in) / ctas);
+#endif
             }
             __syncwarp();
             if (++b == p.nb2) {
@@ -551,11 +553,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas) {
+#ifdef Q8G_DW_TRACE
             const long long ck0 = clock64();
+#endif
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
+#ifdef Q8G_DW_TRACE
             const long long ck1 = clock64();
+#endif
             ptx::mbar_wait(full_bar(b), ph);
             ptx::tc_fence_after();
+#ifdef Q8G_DW_TRACE
+            // debug (tools/dw_trace.py, -DQ8G_DW_TRACE builds): cycles per wait and per loop
             const long long ck2 = clock64();
             if (lane == 0 && p.trace && blockIdx.x == 0 && (k - cta_in) / ctas < 64) {
                 const int u = (k - cta_in) / ctas;
@@ -563,9 +571,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 p.trace[8192 + 25 * 64 + u] = (unsigned long long)(ck2 - ck1);
                 p.trace[8192 + 26 * 64 + u] = (unsigned long long)ck0;
             }
+#endif
             const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride) >> 4);  // TMEM lane m = output column m
             if (ptx::elect_one()) {
+#ifdef Q8G_DW_TRACE  // debug builds only: these stamps in the issue loop cost C4 ~2 us even when off
                 dw_stamp(p, 1, (k - cta_in) / ctas);
+#endif
                 // halo row i = input row r0 - 1 + i feeds output row r0 + 1 with
                 // tap row kh = i - 1 and output row r0 with kh = i:
                 //   i = 0: r0 (kh 0)               N = 64 into slot 1
@@ -592,7 +603,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                         }
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
+#ifdef Q8G_DW_TRACE
                 dw_stamp(p, 2, (k - cta_in) / ctas);
+#endif
             }
             __syncwarp();
             if (++b == p.nb2) {
@@ -647,7 +660,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             __syncwarp();
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
+#ifdef Q8G_DW_TRACE
             if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
+#endif
             const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + j * 128 + (1 - r) * 64);
             // all 32 channels of this warp's tile out of TMEM first, then hand the
             // accumulator buffer back to the MMA warp before the requant math
@@ -662,7 +677,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             __syncwarp();
             if (lane == 0) {
                 ptx::mbar_arrive(tempty_bar(acc));
-                dw_stamp(p, 7 + ew, ui);  // debug trace: this warp released the accumulator
+#ifdef Q8G_DW_TRACE
+                dw_stamp(p, 7 + ew, ui);  // this warp released the accumulator
+#endif
             }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {  // 16 channels at a time
@@ -706,7 +723,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                     "r"(c0 + 32 * j), "r"(quarter * 32), "r"(oh), "r"(n), "r"(stg)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#ifdef Q8G_DW_TRACE
                 if (ew == 0) dw_stamp(p, 4, ui);
+#endif
             }
             if (++acc == 2) {
                 acc = 0;
