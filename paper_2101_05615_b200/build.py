@@ -16,11 +16,15 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-# Q8G_CHECKED=1: the checked library (device-side bounds / layout assertions,
-# Q8G_CHECK in ptx.cuh) from its own object directory, linked to the same
-# libq8g_b200.so name so the package and the tests load it unchanged
+# Variants, each from its own object directory and linked to the same
+# libq8g_b200.so name so the package and the tests load them unchanged:
+#   Q8G_CHECKED=1  device-side bounds / layout assertions (Q8G_CHECK, ptx.cuh);
+#   Q8G_TRACE=1    the phase-trace stamps the tools/*_trace.py probes read.
+#                  The production build compiles them out: even disabled at
+#                  run time their branches cost C4 ~9 %.
 CHECKED = os.environ.get("Q8G_CHECKED") == "1"
-BUILD = PKG / ("_build_checked" if CHECKED else "_build")
+TRACE = os.environ.get("Q8G_TRACE") == "1"
+BUILD = PKG / ("_build" + ("_checked" if CHECKED else "") + ("_trace" if TRACE else ""))
 LIB = PKG / "libq8g_b200.so"
 ROOT = PKG.parent
 
@@ -31,7 +35,7 @@ NVFLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
     "-Xptxas", "-warn-spills",
     f"-I{ROOT / 'include'}",
-] + (["-DQ8G_CHECKED=1"] if CHECKED else [])
+] + (["-DQ8G_CHECKED=1"] if CHECKED else []) + (["-DQ8G_TRACE=1"] if TRACE else [])
 
 
 def _sources():
@@ -76,7 +80,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    for d in {PKG / "_build", PKG / "_build_checked"} - {BUILD}:  # the other object set is stale now
+    for d in set(PKG.glob("_build*")) - {BUILD}:  # the other object sets are stale now
         (d / "linked").unlink(missing_ok=True)
     stamp.write_text(str(LIB.stat().st_mtime_ns))
     return LIB

@@ -85,20 +85,24 @@ struct CvParams {
 // 5 MMA warp past tempty, 6 past full; [8192+320]
 // = prologue done, [8192+321] = kernel entry
 __device__ __forceinline__ void cv_stamp(const CvParams& p, int which, int i) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0 && i < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[which < 5 ? 8192 + which * 64 + i : 9216 + (which - 5) * 64 + i] = t;
     }
+#endif
 }
 
 // CTA 0 prologue stamps [9344 + k]: 0 barriers/image issued (after 1), 1 guards zeroed, 2 TMEM allocated
 __device__ __forceinline__ void cv_pstamp(const CvParams& p, int k) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[9344 + k] = t;
     }
+#endif
 }
 
 // unit ring (see UNIT_RING): tag = local unit index, value = id + 1 (0: none)
@@ -262,12 +266,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L.tmemptr_off);
     const uint32_t img_bar = bar0 + 8u * (2 * MAX_BUF + 2 * MAX_ACC);
     ptx::griddep_launch_dependents();
+#ifdef Q8G_TRACE
     if (threadIdx.x == 0 && p.trace && blockIdx.x < 160) {  // per-CTA entry stamp
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (blockIdx.x == 0) p.trace[8192 + 321] = t;
         p.trace[8704 + blockIdx.x] = t;
     }
+#endif
 
     // ---- guard bands, barriers, then everything overlaps: the producer
     // streams halos while the operand image (B = [weights | ones] + tap weight
@@ -316,11 +322,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     const uint32_t tmem_base = *tmem_ptr;
     // PDL: x is read (producer) and y written (epilogue) only after
     // griddepcontrol.wait; the MMA warp touches only smem / TMEM
+#ifdef Q8G_TRACE
     if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8192 + 320] = t;
     }
+#endif
 
     if (warp == W_PROD) {
         // ------------------------------------------------ halo producer
@@ -561,11 +569,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
                     if (k < nchunk) ptx::tmem_ld_32x32b_x16(lane_base + (uint32_t)(ch0 + 16 * k), v4[k]);
                 ptx::tmem_ld_wait();
                 if (ch0 == 0) rowsum = (int32_t)rs[0];
+#ifdef Q8G_TRACE
                 if (ch0 == 0 && quarter == 0 && lane == 0 && p.trace && blockIdx.x == 0 && i < 64) {
                     unsigned long long tt;  // debug: TMEM loads landed
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
                     p.trace[8192 + 384 + i] = tt;
                 }
+#endif
                 process(v4, nchunk, ch0, rowsum, cls, valid, pix);
             }
             ptx::tc_fence_before();
@@ -582,11 +592,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI_WARPS, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem_base);
     }
+#ifdef Q8G_TRACE
     if (threadIdx.x == 0 && p.trace && blockIdx.x < 160) {  // per-CTA exit stamp
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8704 + 160 + blockIdx.x] = t;
     }
+#endif
 }
 
 CvParams make_params(const ConvArgs& a) {

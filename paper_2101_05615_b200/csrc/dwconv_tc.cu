@@ -70,11 +70,13 @@ struct DwParams {
 // CTA 0, unit i < 64: [8192 + 64*which + i]; which: 0 halo TMA issued, 1 halo
 // landed (MMA), 2 MMAs issued, 3 epilogue got the accumulators, 4 epilogue done
 __device__ __forceinline__ void dw_stamp(const DwParams& p, int which, int i) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0 && i < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8192 + which * 64 + i] = t;
     }
+#endif
 }
 
 __host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 ptx::mbar_arrive_expect_tx(full_bar(b), halo_bytes);
                 // box {64 ch, W+2 px, R2+2 rows, 1} at (c0, col -1, row rb*R2-1, image n)
                 tma_load_4d(base + L.halo_off + b * L.halo_stride, &tmap_x, c0, -1, rb * R2 - 1, n, full_bar(b));
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
                 dw_stamp(p, 0, (k - cta_in) / ctas);
 #endif
             }
@@ -553,17 +555,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
         int b = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int k = cta_in; k < p.units_blk; k += ctas) {
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
             const long long ck0 = clock64();
 #endif
             ptx::mbar_wait(tempty_bar(acc), aph ^ 1);
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
             const long long ck1 = clock64();
 #endif
             ptx::mbar_wait(full_bar(b), ph);
             ptx::tc_fence_after();
-#ifdef Q8G_DW_TRACE
-            // debug (tools/dw_trace.py, -DQ8G_DW_TRACE builds): cycles per wait and per loop
+#ifdef Q8G_TRACE
+            // debug (tools/dw_trace.py, -DQ8G_TRACE builds): cycles per wait and per loop
             const long long ck2 = clock64();
             if (lane == 0 && p.trace && blockIdx.x == 0 && (k - cta_in) / ctas < 64) {
                 const int u = (k - cta_in) / ctas;
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
 #endif
             const uint64_t ahalo = a0 + ((base + L.halo_off + b * L.halo_stride) >> 4);  // TMEM lane m = output column m
             if (ptx::elect_one()) {
-#ifdef Q8G_DW_TRACE  // debug builds only: these stamps in the issue loop cost C4 ~2 us even when off
+#ifdef Q8G_TRACE  // debug builds only: these stamps in the issue loop cost C4 ~2 us even when off
                 dw_stamp(p, 1, (k - cta_in) / ctas);
 #endif
                 // halo row i = input row r0 - 1 + i feeds output row r0 + 1 with
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                         }
                 ptx::tc_commit(empty_bar(b));
                 ptx::tc_commit(tfull_bar(acc));
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
                 dw_stamp(p, 2, (k - cta_in) / ctas);
 #endif
             }
@@ -617,6 +619,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 aph ^= 1;
             }
         }
+#ifdef Q8G_TRACE
     } else if (warp == EPI64 + 2 && p.trace) {
         // debug trace only: the time each halo actually lands (the MMA warp's
         // own stamp also includes its wait for a free accumulator)
@@ -630,6 +633,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                 ph ^= 1;
             }
         }
+#endif
     } else if (warp < EPI64) {
         // ------------------------------------------------ requant epilogue
         ptx::griddep_wait();  // y may be read / written by the previous grid
@@ -660,7 +664,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             __syncwarp();
             ptx::mbar_wait(tfull_bar(acc), aph);
             ptx::tc_fence_after();
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
             if (ew == 0 && lane == 0) dw_stamp(p, 3, ui);
 #endif
             const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + j * 128 + (1 - r) * 64);
@@ -677,7 +681,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
             __syncwarp();
             if (lane == 0) {
                 ptx::mbar_arrive(tempty_bar(acc));
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
                 dw_stamp(p, 7 + ew, ui);  // this warp released the accumulator
 #endif
             }
@@ -723,7 +727,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI64, 1)
                     "r"(c0 + 32 * j), "r"(quarter * 32), "r"(oh), "r"(n), "r"(stg)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-#ifdef Q8G_DW_TRACE
+#ifdef Q8G_TRACE
                 if (ew == 0) dw_stamp(p, 4, ui);
 #endif
             }

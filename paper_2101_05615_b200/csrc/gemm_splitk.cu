@@ -106,18 +106,22 @@ __device__ __forceinline__ void wait_a_ready(const uint32_t* flag, uint32_t epoc
 // 5 past the exchange's cluster barrier, 6 exchange stores issued, 7 done;
 // per-k-block stamps of CTA 0
 __device__ __forceinline__ void sk_stamp(const SkParams& p, int slot) {
+#ifdef Q8G_TRACE
     if (p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace_cta[blockIdx.x * 8 + slot] = t;
     }
+#endif
 }
 __device__ __forceinline__ void sk_kb(const SkParams& p, int which, int i) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0 && i < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8192 + which * 64 + i] = t;
     }
+#endif
 }
 
 __device__ __forceinline__ void cluster_arrive_release() {

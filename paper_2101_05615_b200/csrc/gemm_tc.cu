@@ -73,20 +73,24 @@ struct TcParams {
 };
 
 __device__ __forceinline__ void trace_stamp(const TcParams& p, int slot) {
+#ifdef Q8G_TRACE
     if (p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[blockIdx.x * 8 + slot] = t;
     }
+#endif
 }
 // per-k-block stamps of CTA 0's first tile: [8192 + kb] producer issue,
 // [8192 + 64 + kb] MMA saw the stage land, [8192 + 128 + kb] MMA issued
 __device__ __forceinline__ void trace_kb(const TcParams& p, int which, int kb) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0 && kb < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8192 + which * 64 + kb] = t;
     }
+#endif
 }
 
 constexpr int EPI_COLS = 16;  // columns per tcgen05.ld in the epilogue

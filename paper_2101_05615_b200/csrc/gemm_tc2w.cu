@@ -142,10 +142,12 @@ __device__ __forceinline__ void tw_clk(const Tc2wParams& p, int end) {
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
         g_tc2w_clock[end] = c;
         g_tc2w_clock[2 + end] = t;
+#ifdef Q8G_TRACE
         if (p.trace) {
             p.trace[10200 + end] = c;
             p.trace[10202 + end] = t;
         }
+#endif
     }
 }
 // CTA 0, per tile ti < 16: [9216 + 8 * ti + k] (tools/tc2w_tiles.py): MMA
@@ -153,22 +155,26 @@ __device__ __forceinline__ void tw_clk(const Tc2wParams& p, int end) {
 // committed; epilogue warp 4: 4 / 6 tfull[0] / tfull[1] seen, 5 / 7 half 0 / 1
 // drained into registers
 __device__ __forceinline__ void tw_tile(const Tc2wParams& p, int k, int ti) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0 && ti < 16) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[9216 + 8 * ti + k] = t;
     }
+#endif
 }
 
 // CTA 0 epilogue warp 4, per tile ti < 16: [9472 + 8 * ti + k], k = 6 + h:
 // half h's row sums in hand, 3h + 0: half h round 0 requantized, 3h + 1: round 1 staging tile free, 3h + 2:
 // round 1 requantized (tools/tc2w_tiles.py)
 __device__ __forceinline__ void tw_epi(const Tc2wParams& p, int k, int ti) {
+#ifdef Q8G_TRACE
     if (p.trace && blockIdx.x == 0 && ti < 16) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[9472 + 8 * ti + k] = t;
     }
+#endif
 }
 
 __device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* m, int c0, int c1,
