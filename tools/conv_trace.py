@@ -1,6 +1,10 @@
 """Per-unit timeline of CTA 0 in the tensor-core conv3x3 kernel (debug;
 Q8G_TC_TRACE=1), C3 shape.  Columns: halo issued / MMA start / MMA committed
-/ epilogue start / epilogue done, us from the first stamp; plus prologue end."""
+/ epilogue start / epilogue done, us from the first stamp; plus prologue end.
+Needs the trace build of the library: Q8G_TRACE=1 python -c "from
+paper_2101_05615_b200 import build as b; b.build()" (the production build
+compiles the stamps out; rebuild without Q8G_TRACE afterwards).
+"""
 import ctypes as C
 import os
 import sys

@@ -3,7 +3,11 @@ Q8G_TC_TRACE=1), in us from the first stamp: halo TMA issued, halo landed
 (an idle warp waits on its full barrier), accumulator free and both waits
 passed (MMA warp), MMAs issued, epilogue start / done; then each epilogue
 warp's accumulator release, and the MMA warp's clock64 cycles per wait and
-per loop iteration (what paces the kernel: the MMA issue loop)."""
+per loop iteration (what paces the kernel: the MMA issue loop).
+Needs the trace build of the library: Q8G_TRACE=1 python -c "from
+paper_2101_05615_b200 import build as b; b.build()" (the production build
+compiles the stamps out; rebuild without Q8G_TRACE afterwards).
+"""
 import ctypes as C
 import os
 import sys

@@ -3,7 +3,11 @@ GEMM (gemm_tc2w.cu; debug, Q8G_TC_TRACE=1) at the C2 shape, us from the
 first stamp: when the MMA issuer got each accumulator half back (tempty),
 when it committed each half (tfull), when the epilogue saw each half full
 and when it had drained it into registers.  --raw / --zpb0 select the
-epilogue; the last launch of --reps back-to-back launches is shown."""
+epilogue; the last launch of --reps back-to-back launches is shown.
+Needs the trace build of the library: Q8G_TRACE=1 python -c "from
+paper_2101_05615_b200 import build as b; b.build()" (the production build
+compiles the stamps out; rebuild without Q8G_TRACE afterwards).
+"""
 import ctypes as C
 import os
 import sys

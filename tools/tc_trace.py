@@ -4,6 +4,9 @@ Stamps (globaltimer ns) per CTA: 0 entry, 1 prologue done, 2 first TMA
 issued, 3 first stage landed (MMA), 4 last MMA commit, 5 epilogue start,
 6 epilogue done, 7 exit.  Prints min/median/max of each relative to the
 earliest entry over all CTAs.
+Needs the trace build of the library: Q8G_TRACE=1 python -c "from
+paper_2101_05615_b200 import build as b; b.build()" (the production build
+compiles the stamps out; rebuild without Q8G_TRACE afterwards).
 """
 import argparse
 import ctypes as C
