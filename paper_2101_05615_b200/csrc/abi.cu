@@ -966,12 +966,18 @@ int run_host_pipeline(int device, cudaStream_t s, const HostPipeSpec& sp, F comp
 // images per chunk of the host-view conv / depthwise pipelines: imgs / parts
 // (Q8G_HOST_CHUNK_IMG overrides, A/B)
 static int host_chunk_images(int imgs, int parts, size_t img_bytes) {
-    (void)img_bytes;
     static const int env = [] {
         const char* e = getenv("Q8G_HOST_CHUNK_IMG");
         return e ? atoi(e) : 0;
     }();
     if (env > 0) return env;
+    // at least ~2 MB per chunk: each chunk costs ~20 us of host-side API calls
+    // (two copies, events, the launch), which small chunks cannot amortize
+    // (C3, 6.4 MB each way: 4-image chunks 270-416 us per call, 16-image
+    // chunks 240 us)
+    const size_t total = img_bytes * (size_t)imgs;
+    const int by_size = (int)std::max<size_t>(1, total / ((size_t)2 << 20));
+    parts = std::max(1, std::min(parts, by_size));
     return std::max(1, (imgs + parts - 1) / parts);
 }
 

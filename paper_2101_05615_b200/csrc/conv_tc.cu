@@ -733,8 +733,16 @@ cudaError_t launch_conv3x3_tc(const ConvArgs& a, cudaStream_t s) {
     const int mode = a.raw ? 0 : (a.ep->rounding == Q8G_ROUND_F32_RNE ? 1 : 2);
     const int ks = a.c / 32;
     const int threads = 128 + 32 * EPI_WARPS;
+    // the dynamic-smem attribute once per (kernel variant, device): the
+    // attribute call costs host time on every host-view chunk otherwise
+    static bool attr[3][3][64] = {};
+    const int mi = mode, ki = ks == 1 ? 0 : ks == 2 ? 1 : 2;
     auto go = [&](auto kern) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        cudaError_t e = cudaSuccess;
+        if (dev >= 64 || !attr[mi][ki][dev]) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+            if (e == cudaSuccess && dev < 64) attr[mi][ki][dev] = true;
+        }
         if (e == cudaSuccess) e = launch_with_pdl(kern, dim3(grid), dim3(threads), L.total, s, tmap, p);
         return e;
     };
