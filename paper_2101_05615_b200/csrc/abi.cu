@@ -571,7 +571,7 @@ static int gemm_common(const uint8_t* a, int m, int k, int lda, const q8g_packed
     // goes from the local C to each peer by the copy engines, stream-ordered
     for (int d = 0; d < n_peers && !peers_written; ++d) {
         e = cudaMemcpy2DAsync(peers[d], (size_t)ldc, g.c, (size_t)ldc, (size_t)pb->n, (size_t)g.rows,
-                              cudaMemcpyDeviceToDevice, s);
+                              cudaMemcpyDefault, s);  // UVA: also across devices without peer access
         if (e != cudaSuccess) return cuda_fail(e, "peer copy");
         count_launch(kFamPeerCopy);
     }
